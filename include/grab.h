@@ -1,0 +1,179 @@
+/*
+ * grab.h -- C ABI of the B200-native GRAB-ANNS range-filtered graph index.
+ *
+ * The reference (/root/reference/pkg/src/bucketann, pure Python + numpy) has no
+ * FFI: callers use the Python functions re-exported by bucketann/__init__.py:3-44.
+ * Each entry point below replaces one of those functions; the Python package
+ * paper_2604_16402_b200 binds them with ctypes and rebuilds the reference's
+ * return types (SearchResult, BuildReport, InsertReport, GraphIndex views).
+ *
+ * Conventions
+ *  - plain pointers + sizes; no torch types.
+ *  - ids crossing the ABI are reference SLOT ids (physical row order in the
+ *    reference's VectorStore, layout.py:22-79); the device keeps its own
+ *    bucket-slab physical order internally.
+ *  - `mem` selects where pointer arguments live: GRAB_MEM_HOST (copied by the
+ *    library, synchronous) or GRAB_MEM_DEVICE (device pointers, enqueued on
+ *    `stream`, asynchronous).
+ *  - every call returns GRAB_OK or a GRAB_ERR_* code; grab_last_error() gives
+ *    the message (thread-local). Codes map 1:1 to the reference's exceptions
+ *    (core.py:17-22, layout.py:59-63,200-207).
+ */
+#ifndef GRAB_H_
+#define GRAB_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GRAB_API __attribute__((visibility("default")))
+#else
+#define GRAB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRAB_OK 0
+#define GRAB_ERR_VALUE 1     /* ValueError */
+#define GRAB_ERR_DIMENSION 2 /* DimensionMismatchError (ValueError) */
+#define GRAB_ERR_CAPACITY 3  /* CapacityError (RuntimeError) */
+#define GRAB_ERR_CUDA 4      /* device failure */
+#define GRAB_ERR_STATE 5     /* e.g. operation on a never-built index */
+
+#define GRAB_MEM_HOST 0
+#define GRAB_MEM_DEVICE 1
+
+#define GRAB_SENTINEL 0xFFFFFFFFu /* empty adjacency slot, layout.py:19 */
+#define GRAB_LIVE_ALL 0xFFFFFFFFFFFFFFFFull
+
+#define GRAB_STRATEGY_QUANTILE 0
+#define GRAB_STRATEGY_WIDTH 1
+
+typedef struct grab_index grab_index;
+
+/* BuildParams (core.py:85-118) */
+typedef struct {
+  uint32_t k_max, k_local, bucket_capacity, _pad;
+  double proximal_fraction, proximal_window, alpha;
+  uint64_t rng_seed;
+} grab_build_params;
+
+/* SearchParams minus the range (core.py:121-147); seed_count 0 = min(itopk, 32) */
+typedef struct {
+  uint32_t k, itopk, search_width, max_iterations, seed_count, _pad;
+} grab_search_params;
+
+/* SearchStats (searcher.py:22-31) + `expanded` (frontier nodes popped) */
+typedef struct {
+  uint32_t iterations, dist_evals, seed_evals, gathered;
+  uint32_t in_range_new, precheck_rejected, seed_attempts, expanded;
+} grab_search_stats;
+
+/* BuildReport (builder.py:63-76) */
+typedef struct {
+  uint64_t n;
+  uint32_t m, isolated_nodes;
+  double phase1_seconds, phase2_seconds, fuse_seconds, total_seconds;
+  double cross_bucket_edge_ratio;
+} grab_build_report;
+
+/* InsertReport (updater.py:31-46); rewired rows via grab_last_rewired() */
+typedef struct {
+  uint64_t batch_size, bulk_built, forward_accepted, forward_rejected;
+  uint64_t reverse_accepted, reverse_rejected, evictions_necessary, evictions_redundant;
+  uint64_t forced_links, n_rewired;
+  double wall_time_s;
+} grab_insert_report;
+
+typedef struct {
+  uint64_t count, capacity;
+  uint32_t dim, k_max, k_local, m;
+  int32_t built;
+  uint32_t _pad;
+  uint64_t phys_capacity, device_bytes;
+} grab_info_t;
+
+/* grab_read / grab_write array selectors (slot space unless noted) */
+#define GRAB_ARR_X 0          /* f32 [count x dim] */
+#define GRAB_ARR_SCALARS 1    /* f32 [count] */
+#define GRAB_ARR_ADJ 2        /* u32 [count x k_max], slot ids / SENTINEL */
+#define GRAB_ARR_I2B 3        /* i32 [count] (M_I2B) */
+#define GRAB_ARR_BOUNDARIES 4 /* f32 [m+1] */
+#define GRAB_ARR_B2I_OFFSETS 5 /* u64 [m+1]: bucket b members are B2I_FLAT[off[b]:off[b+1]] */
+#define GRAB_ARR_B2I_FLAT 6   /* u32 [count]: M_B2I lists concatenated, insertion order */
+
+/* ---- lifecycle (create_index, layout.py:250-257) ---- */
+GRAB_API int grab_create(int device, uint32_t dim, uint64_t capacity, const grab_build_params* params,
+                grab_index** out);
+GRAB_API void grab_destroy(grab_index* h);
+GRAB_API const char* grab_last_error(void);
+GRAB_API int grab_get_info(const grab_index* h, grab_info_t* out);
+GRAB_API int grab_sync(grab_index* h);
+
+/* ---- build_index (builder.py:503-548) over host or device rows ---- */
+GRAB_API int grab_build(grab_index* h, const float* vectors, const float* scalars, uint64_t n, int strategy,
+               uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report);
+
+/* ---- insert_batch (updater.py:154-263) ---- */
+GRAB_API int grab_insert(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids,
+                uint64_t b, uint32_t search_itopk, uint32_t mem, grab_insert_report* report);
+GRAB_API int grab_last_rewired(const grab_index* h, uint32_t* out, uint64_t cap, uint64_t* n_out);
+
+/* ---- search / search_batch (searcher.py:156-248) ----
+ * Query i uses range [lower[i*range_stride], upper[i*range_stride]] (stride 0 =
+ * one shared range, as search_batch) and RNG seed seeds[i] when `seeds` is
+ * non-NULL, else derive_query_seed(seed_base, ordinal0 + i) (searcher.py:85-87).
+ * live_count = GRAB_LIVE_ALL uses the published count. Outputs: k slots
+ * (int64, -1 padded) and squared distances (f64) per query, ascending by
+ * (dist, slot); out_counts[i] = result length; out_stats optional. */
+GRAB_API int grab_search(const grab_index* h, const float* queries, uint64_t nq, const double* lower,
+                const double* upper, uint64_t range_stride, const grab_search_params* params,
+                const uint64_t* seeds, uint64_t seed_base, uint64_t ordinal0, uint64_t live_count,
+                int64_t* out_slots, double* out_dists, uint32_t* out_counts,
+                grab_search_stats* out_stats, uint32_t mem, void* stream);
+
+/* ---- brute_force_search (evaluate.py:22-44): exact (dist, slot) top-k ---- */
+GRAB_API int grab_brute_force(const grab_index* h, const float* queries, uint64_t nq, const double* lower,
+                     const double* upper, uint64_t range_stride, uint32_t k, uint64_t live_count,
+                     int64_t* out_slots, double* out_dists, uint32_t* out_counts, uint32_t mem,
+                     void* stream);
+
+/* ---- bucket selection: intersecting_buckets / bucket_ids_of (layout.py:157-174) ---- */
+GRAB_API int grab_bucket_select(const grab_index* h, const double* lower, const double* upper, uint64_t n,
+                       int32_t* out_lo, int32_t* out_hi, uint32_t mem, void* stream);
+GRAB_API int grab_bucket_ids(const grab_index* h, const float* scalars, uint64_t n, int32_t* out,
+                    uint32_t mem, void* stream);
+
+/* stateless variants over explicit boundaries f32[m+1] (host pointers) */
+GRAB_API int grab_bucket_ids_raw(const float* boundaries, uint32_t m, const float* scalars, uint64_t n,
+                                 int32_t* out);
+GRAB_API int grab_bucket_select_raw(const float* boundaries, uint32_t m, const double* lower,
+                                    const double* upper, uint64_t n, int32_t* out_lo, int32_t* out_hi);
+
+/* ---- sq_distances (core.py:25-38): f64-accumulated squared L2, host pointers ----
+ * Same reduction tree as the search / brute-force kernels (bit-identical). */
+GRAB_API int grab_sq_distances(const float* q, const float* rows, uint64_t n, uint32_t dim, double* out);
+
+/* ---- state import / export (GraphIndex <-> device layout; dataio.py:111-187) ---- */
+GRAB_API int grab_import(grab_index* h, uint64_t n, const float* X, const float* scalars,
+                const uint32_t* adjacency, const float* boundaries, uint32_t m, const int32_t* i2b,
+                const uint32_t* b2i_flat, const uint64_t* b2i_offsets);
+GRAB_API int grab_read(const grab_index* h, int what, uint64_t start, uint64_t count, void* out);
+
+/* ---- pruning primitives on explicit inputs (updater.py:49-123) ---- */
+/* select_neighbors: rows X [n_rows x dim] (host), candidates (slot, f64 dist)
+ * sorted ascending; fresh[i] != 0 marks Q_new. Returns accepted slots. */
+GRAB_API int grab_select_neighbors(const float* X, uint64_t n_rows, uint32_t dim, int64_t target,
+                          const int64_t* cand_slots, const double* cand_dists,
+                          const uint8_t* cand_fresh, uint32_t n_cand, uint32_t row_capacity,
+                          double alpha, int64_t* out_accepted, uint32_t* n_accepted);
+/* try_rewire on one adjacency row (k_max entries, slot ids) */
+GRAB_API int grab_try_rewire(const float* X, uint64_t n_rows, uint32_t dim, uint32_t* row, uint32_t k_max,
+                    uint32_t v, uint32_t q, double sq_dvq, double alpha, uint32_t k_local,
+                    int32_t* accepted, int32_t* evicted_pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAB_H_ */

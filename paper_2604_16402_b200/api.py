@@ -1,0 +1,248 @@
+"""Operations of the drop-in surface, each one call into libgrab.
+
+Reference functions replaced (paths under /root/reference/pkg/src/bucketann):
+  search / search_batch          searcher.py:156-248
+  brute_force_search             evaluate.py:22-44
+  bucket_of / intersecting_buckets / bucket_ids_of   layout.py:157-174
+  build_index                    builder.py:503-548
+  insert_batch                   updater.py:154-263
+  select_neighbors / try_rewire  updater.py:49-123
+
+Inputs may be numpy arrays (host; copied by the library) or CUDA torch tensors
+(device-resident; no host round trip).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .graph import BucketMeta, GraphIndex, create_index
+from .params import BuildParams, DimensionMismatchError, RangePredicate, SearchParams
+
+
+@dataclass
+class SearchStats:
+    """searcher.py:22-31 (+ ``expanded``: frontier nodes popped)."""
+
+    iterations: int = 0
+    dist_evals: int = 0
+    seed_evals: int = 0
+    gathered: int = 0
+    in_range_new: int = 0
+    precheck_rejected: int = 0
+    seed_attempts: int = 0
+    expanded: int = 0
+    elapsed_s: float = 0.0
+
+
+@dataclass
+class SearchResult:
+    """searcher.py:34-49: ascending (distance, slot); ``truncated`` when 0 < len < k."""
+
+    slots: np.ndarray
+    sq_dists: np.ndarray
+    truncated: bool
+    stats: SearchStats = field(default_factory=SearchStats)
+
+    def __len__(self) -> int:
+        return len(self.slots)
+
+
+@dataclass
+class BatchResult:
+    """Array form of a query batch: slots/dists [nq, k] (-1 / NaN padded), counts, stats."""
+
+    slots: np.ndarray
+    dists: np.ndarray
+    counts: np.ndarray
+    stats: np.ndarray | None
+    elapsed_s: float
+
+    def to_results(self, k: int) -> list[SearchResult]:
+        out = []
+        per = self.elapsed_s / max(len(self.counts), 1)
+        for i in range(len(self.counts)):
+            c = int(self.counts[i])
+            st = SearchStats(**{f: int(self.stats[i][f]) for f in L.STAT_FIELDS}, elapsed_s=per) \
+                if self.stats is not None else SearchStats(elapsed_s=per)
+            out.append(SearchResult(self.slots[i, :c].copy(), self.dists[i, :c].copy(), 0 < c < k, st))
+        return out
+
+
+def _is_dev(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _live(live_count) -> int:
+    return L.LIVE_ALL if live_count is None else int(live_count)
+
+
+def _search_params_c(params: SearchParams) -> L.SearchParamsC:
+    return L.SearchParamsC(k=params.k, itopk=params.itopk, search_width=params.search_width,
+                           max_iterations=params.max_iterations, seed_count=params.seed_count or 0)
+
+
+def search_arrays(index: GraphIndex, queries, lower, upper, params: SearchParams, *, seeds=None,
+                  seed_base: int | None = None, ordinal0: int = 0, live_count=None, stats: bool = True,
+                  stream=None) -> BatchResult:
+    """Batched filtered search with per-query ranges.
+
+    ``lower``/``upper``: per-query bounds (arrays of length nq) or scalars (one
+    shared range). Per-query RNG seed = ``seeds[i]`` if given, else
+    derive_query_seed(seed_base, ordinal0 + i) (searcher.py:85-87; seed_base
+    defaults to params.rng_seed, i.e. search_batch semantics).
+    """
+    dev = _is_dev(queries)
+    if dev:
+        import torch
+        Q = queries.contiguous()
+        nq, d = Q.shape
+        lo = torch.as_tensor(lower, dtype=torch.float64, device=Q.device).reshape(-1).contiguous()
+        hi = torch.as_tensor(upper, dtype=torch.float64, device=Q.device).reshape(-1).contiguous()
+        sd = None if seeds is None else torch.as_tensor(seeds, dtype=torch.uint64, device=Q.device).contiguous()
+        k = params.k
+        slots = torch.empty((nq, k), dtype=torch.int64, device=Q.device)
+        dists = torch.empty((nq, k), dtype=torch.float64, device=Q.device)
+        counts = torch.empty(nq, dtype=torch.int32, device=Q.device)
+        st = torch.empty((nq, len(L.STAT_FIELDS)), dtype=torch.int32, device=Q.device) if stats else None
+        mem = L.MEM_DEVICE
+        s_ptr = stream if stream is not None else torch.cuda.current_stream(Q.device).cuda_stream
+    else:
+        Q = np.ascontiguousarray(queries, dtype=np.float32)
+        if Q.ndim == 1:
+            Q = Q.reshape(1, -1)
+        nq, d = Q.shape
+        lo = np.ascontiguousarray(np.atleast_1d(np.asarray(lower, dtype=np.float64)))
+        hi = np.ascontiguousarray(np.atleast_1d(np.asarray(upper, dtype=np.float64)))
+        sd = None if seeds is None else np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        k = params.k
+        slots = np.empty((nq, k), dtype=np.int64)
+        dists = np.empty((nq, k), dtype=np.float64)
+        counts = np.empty(nq, dtype=np.uint32)
+        st = np.empty(nq, dtype=L.STATS_DTYPE) if stats else None
+        mem = L.MEM_HOST
+        s_ptr = None
+    if d != index.dim:
+        raise DimensionMismatchError(f"query dimension {d} vs index dimension {index.dim}")
+    stride = 0 if len(lo) == 1 else 1
+    if len(lo) not in (1, nq) or len(hi) != len(lo):
+        raise ValueError("lower/upper must be scalars or have one entry per query")
+    base = params.rng_seed if seed_base is None else seed_base
+    t0 = time.perf_counter()
+    if nq:
+        L.check(L.lib.grab_search(index.handle, L.ptr(Q), nq, L.ptr(lo), L.ptr(hi), stride,
+                                  C.byref(_search_params_c(params)), L.ptr(sd), int(base), int(ordinal0),
+                                  _live(live_count), L.ptr(slots), L.ptr(dists), L.ptr(counts), L.ptr(st), mem,
+                                  s_ptr))
+    el = time.perf_counter() - t0
+    return BatchResult(slots, dists, counts, st, el)
+
+
+def search(index: GraphIndex, query, params: SearchParams, *, live_count=None) -> SearchResult:
+    """searcher.py:156-233: one query, RNG seeded with params.rng_seed directly."""
+    q = np.asarray(query, dtype=np.float32).reshape(1, -1)
+    r = search_arrays(index, q, params.range.lower, params.range.upper, params,
+                      seeds=np.array([params.rng_seed], dtype=np.uint64), live_count=live_count)
+    return r.to_results(params.k)[0]
+
+
+def search_batch(index: GraphIndex, queries, params: SearchParams, *, live_count=None) -> list[SearchResult]:
+    """searcher.py:236-248: shared range, seeds derive_query_seed(params.rng_seed, i)."""
+    Q = np.asarray(queries, dtype=np.float32)
+    if len(Q) == 0:
+        return []
+    r = search_arrays(index, Q, params.range.lower, params.range.upper, params, live_count=live_count)
+    return r.to_results(params.k)
+
+
+def brute_force_arrays(index: GraphIndex, queries, lower, upper, k: int, live_count=None):
+    """Exact range-filtered top-k for a batch: (slots [nq,k] -1 padded, dists, counts)."""
+    Q = np.ascontiguousarray(queries, dtype=np.float32)
+    if Q.ndim == 1:
+        Q = Q.reshape(1, -1)
+    nq, d = Q.shape
+    if d != index.dim:
+        raise DimensionMismatchError(f"query dimension {d} vs index dimension {index.dim}")
+    lo = np.ascontiguousarray(np.atleast_1d(np.asarray(lower, dtype=np.float64)))
+    hi = np.ascontiguousarray(np.atleast_1d(np.asarray(upper, dtype=np.float64)))
+    stride = 0 if len(lo) == 1 else 1
+    slots = np.empty((nq, k), dtype=np.int64)
+    dists = np.empty((nq, k), dtype=np.float64)
+    counts = np.empty(nq, dtype=np.uint32)
+    if nq:
+        L.check(L.lib.grab_brute_force(index.handle, L.ptr(Q), nq, L.ptr(lo), L.ptr(hi), stride, k,
+                                       _live(live_count), L.ptr(slots), L.ptr(dists), L.ptr(counts), L.MEM_HOST,
+                                       None))
+    return slots, dists, counts
+
+
+def brute_force_search(store, query, k: int, rng: RangePredicate, live_count=None):
+    """evaluate.py:22-44 over the index's rows (``store`` = index.store or the index)."""
+    index = store._ix if hasattr(store, "_ix") else store
+    s, d, c = brute_force_arrays(index, np.asarray(query, dtype=np.float32).reshape(1, -1), rng.lower, rng.upper,
+                                 k, live_count)
+    n = int(c[0])
+    return s[0, :n].copy(), d[0, :n].copy()
+
+
+def sq_distances(q, rows) -> np.ndarray:
+    """core.py:25-38 on the device: f64-accumulated squared L2 of q to each row.
+
+    Uses the same lane split and reduction tree as the search and brute-force
+    kernels, so a distance returned by search equals sq_distance() bit for bit.
+    """
+    q = np.asarray(q)
+    rows = np.asarray(rows)
+    if rows.ndim != 2 or q.ndim != 1 or rows.shape[1] != q.shape[0]:
+        raise DimensionMismatchError(f"shape mismatch: query {q.shape} vs rows {rows.shape}")
+    qf = np.ascontiguousarray(q, dtype=np.float32)
+    rf = np.ascontiguousarray(rows, dtype=np.float32)
+    out = np.empty(len(rf), dtype=np.float64)
+    if len(rf):
+        L.check(L.lib.grab_sq_distances(L.ptr(qf), L.ptr(rf), len(rf), rf.shape[1], L.ptr(out)))
+    return out
+
+
+def sq_distance(a, b) -> float:
+    """core.py:41-47."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.shape != b.shape or a.ndim != 1:
+        raise DimensionMismatchError(f"shape mismatch: {a.shape} vs {b.shape}")
+    return float(sq_distances(a, b.reshape(1, -1))[0])
+
+
+# ---- bucket selection (layout.py:157-174) -----------------------------------
+def bucket_ids_of(meta, scalars) -> np.ndarray:
+    index = meta if isinstance(meta, GraphIndex) else None
+    s = np.ascontiguousarray(np.atleast_1d(np.asarray(scalars, dtype=np.float32)))
+    out = np.empty(len(s), dtype=np.int32)
+    if len(s) == 0:
+        return out
+    if index is not None:
+        L.check(L.lib.grab_bucket_ids(index.handle, L.ptr(s), len(s), L.ptr(out), L.MEM_HOST, None))
+        return out
+    b = np.ascontiguousarray(meta.boundaries, dtype=np.float32)
+    L.check(L.lib.grab_bucket_ids_raw(L.ptr(b), len(b) - 1, L.ptr(s), len(s), L.ptr(out)))
+    return out
+
+
+def bucket_of(meta, s: float) -> int:
+    return int(bucket_ids_of(meta, np.array([s], dtype=np.float32))[0])
+
+
+def intersecting_buckets(meta, rng: RangePredicate) -> tuple[int, int]:
+    lo = np.array([rng.lower], dtype=np.float64)
+    hi = np.array([rng.upper], dtype=np.float64)
+    a = np.empty(1, dtype=np.int32)
+    b = np.empty(1, dtype=np.int32)
+    if isinstance(meta, GraphIndex):
+        L.check(L.lib.grab_bucket_select(meta.handle, L.ptr(lo), L.ptr(hi), 1, L.ptr(a), L.ptr(b), L.MEM_HOST, None))
+    else:
+        bd = np.ascontiguousarray(meta.boundaries, dtype=np.float32)
+        L.check(L.lib.grab_bucket_select_raw(L.ptr(bd), len(bd) - 1, L.ptr(lo), L.ptr(hi), 1, L.ptr(a), L.ptr(b)))
+    return int(a[0]), int(b[0])

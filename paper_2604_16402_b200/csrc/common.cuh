@@ -1,0 +1,84 @@
+// Shared helpers for the GRAB B200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/grab.h"
+
+namespace grab {
+
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // reference layout.py:19
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+
+// Error carrying one of the GRAB_ERR_* codes; converted at the C-ABI edge.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GRAB_CUDA(call)                                                              \
+  do {                                                                               \
+    cudaError_t e__ = (call);                                                        \
+    if (e__ != cudaSuccess)                                                          \
+      throw ::grab::Error(GRAB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define GRAB_CHECK_LAUNCH() GRAB_CUDA(cudaGetLastError())
+
+// Per-phys-row attribute record: the scalar predicate and the slot id, read
+// together by one 8-byte load during the scalar pre-check.
+struct __align__(8) Attr {
+  float s;
+  uint32_t slot;  // kNoSlot for an unused phys row (headroom)
+};
+
+__host__ __device__ inline uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ float4 ldg_nc_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ Attr ld_attr(const Attr* a, uint32_t p) {
+  uint2 v = __ldg(reinterpret_cast<const uint2*>(a) + p);
+  Attr r;
+  r.s = __uint_as_float(v.x);
+  r.slot = v.y;
+  return r;
+}
+
+// Accumulate (x-q)^2 for one float4 in f64, ascending coordinate order.
+__device__ __forceinline__ double sq4(float4 x, float4 q, double acc) {
+  double a = (double)x.x - (double)q.x;
+  acc = fma(a, a, acc);
+  a = (double)x.y - (double)q.y;
+  acc = fma(a, a, acc);
+  a = (double)x.z - (double)q.z;
+  acc = fma(a, a, acc);
+  a = (double)x.w - (double)q.w;
+  acc = fma(a, a, acc);
+  return acc;
+}
+
+// Butterfly all-reduce, pairing lane i with i^16, ^8, ^4, ^2, ^1. Every
+// distance in this library goes through this tree so a given (q, x) pair has
+// one bit pattern regardless of which kernel computed it.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+// Total order used for every (distance, slot) decision (SPEC tie rule).
+__device__ __forceinline__ bool key_less(double da, uint32_t sa, double db, uint32_t sb) {
+  return da < db || (da == db && sa < sb);
+}
+
+}  // namespace grab

@@ -1,0 +1,25 @@
+// Host-side entry points of the kernel families (one .cu each).
+#pragma once
+#include "index.cuh"
+
+namespace grab {
+
+// bruteforce.cu
+void run_bruteforce(const DevIndex& ix, const float* Q, uint64_t nq, const double* lo, const double* hi,
+                    uint64_t stride, uint32_t k, uint64_t n_live, int64_t* os, double* od, uint32_t* oc,
+                    cudaStream_t st);
+void run_sq_distances(const float* q, const float* rows, uint64_t n, uint32_t dp, double* out, cudaStream_t st);
+// build.cu
+void build_index_device(DevIndex& ix, const float* vectors, const float* scalars, uint64_t n, int strategy,
+                        uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report);
+// insert.cu
+void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
+                         uint32_t search_itopk, uint32_t mem, grab_insert_report* report);
+void select_neighbors_device(const float* X, uint64_t n_rows, uint32_t dim, int64_t target, const int64_t* cand_slots,
+                             const double* cand_dists, const uint8_t* cand_fresh, uint32_t n_cand,
+                             uint32_t row_capacity, double alpha, int64_t* out_accepted, uint32_t* n_accepted);
+void try_rewire_device(const float* X, uint64_t n_rows, uint32_t dim, uint32_t* row, uint32_t k_max, uint32_t v,
+                       uint32_t q, double sq_dvq, double alpha, uint32_t k_local, int32_t* accepted,
+                       int32_t* evicted_pos);
+
+}  // namespace grab

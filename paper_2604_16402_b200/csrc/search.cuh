@@ -1,0 +1,49 @@
+// Search kernel arguments (filtered_beam_search + seed_sample).
+#pragma once
+#include <stdint.h>
+
+#include "index.cuh"
+
+namespace grab {
+
+struct SearchArgs {
+  // index (phys space)
+  const float* X;
+  const Attr* attr;
+  const uint32_t* adj;
+  uint32_t dp, k_max;
+  const float* bound;
+  uint32_t m;
+  const uint32_t* bstart;
+  const uint32_t* bcount;
+  const uint64_t* bcum;
+  uint64_t n_live;
+  // queries (rows padded to dp)
+  const float* Q;
+  const double* lower;
+  const double* upper;
+  uint64_t range_stride;
+  const uint64_t* seeds;
+  uint64_t seed_base, ordinal0;
+  uint32_t k, itopk, width, max_iter, want;
+  // work list / overflow retry
+  const uint32_t* qmap;
+  uint32_t nwork;
+  uint32_t* gtab;
+  uint32_t* ovf_list;
+  uint32_t* ovf_count;
+  // outputs (indexed by query id)
+  int64_t* out_slots;
+  double* out_dists;
+  uint32_t* out_counts;
+  grab_search_stats* out_stats;
+};
+
+struct SearchShape {
+  uint32_t itopk, width, cmax, dsz, vlog2;
+};
+
+SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst);
+void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st);
+
+}  // namespace grab

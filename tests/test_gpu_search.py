@@ -1,0 +1,121 @@
+"""GPU parity: search / brute force / bucket selection through the C ABI versus
+golden vectors frozen from the live reference (tests/golden/make_golden.py)."""
+import numpy as np
+import pytest
+
+from oracle import beam, index_state as ist
+
+pytestmark = pytest.mark.gpu
+
+GRID = [dict(k=10, itopk=128, search_width=4, max_iterations=50),
+        dict(k=10, itopk=32, search_width=1, max_iterations=50),
+        dict(k=5, itopk=64, search_width=2, max_iterations=10),
+        dict(k=16, itopk=256, search_width=4, max_iterations=100)]
+STAT_KEYS = ["iterations", "dist_evals", "seed_evals", "gathered", "in_range_new", "precheck_rejected",
+             "seed_attempts"]
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_2604_16402_b200 as g
+    return g
+
+
+def _compare_grid(g, gi, Q, prefix, gold):
+    for si in range(4):
+        lo, hi = gold[f"{prefix}_sel{si}_lower"], gold[f"{prefix}_sel{si}_upper"]
+        for gidx, p in enumerate(GRID):
+            params = g.SearchParams(**p)
+            res = g.search_arrays(gi, Q, lo, hi, params, seed_base=11)
+            key = f"{prefix}_sel{si}_g{gidx}_"
+            assert np.array_equal(res.counts.astype(np.int32), gold[key + "counts"]), (si, gidx)
+            for i in range(len(Q)):
+                c = int(res.counts[i])
+                assert np.array_equal(res.slots[i, :c], gold[key + "slots"][i, :c]), (si, gidx, i)
+                np.testing.assert_allclose(res.dists[i, :c], gold[key + "dists"][i, :c], rtol=1e-12, atol=0)
+                got = [int(res.stats[i][f]) for f in STAT_KEYS]
+                assert got == gold[key + "stats"][i].tolist(), (si, gidx, i)
+            tr = (res.counts > 0) & (res.counts < p["k"])
+            assert np.array_equal(tr, gold[key + "truncated"])
+        s, d, c = g.brute_force_arrays(gi, Q, lo, hi, 10)
+        want_s = gold[f"{prefix}_sel{si}_bf_slots"]
+        for i in range(len(Q)):
+            n = int(c[i])
+            assert np.array_equal(s[i, :n], want_s[i][want_s[i] >= 0])
+            np.testing.assert_allclose(d[i, :n], gold[f"{prefix}_sel{si}_bf_dists"][i, :n], rtol=1e-12, atol=0)
+
+
+def test_small_index_search_matches_reference(g, golden):
+    gold = golden("small")
+    gi = g.load_index(gold["container"].tobytes(), g.BuildParams(k_max=16, k_local=8, bucket_capacity=250))
+    Q, _ = ist.gen_synthetic(64, 8, "clusters", rng_seed=1)
+    _compare_grid(g, gi, Q + np.float32(0.01), "s", gold)
+
+
+def test_mid_index_search_matches_reference(g, golden):
+    gold = golden("mid")
+    gi = g.load_index(gold["container"].tobytes())
+    V, _ = ist.gen_synthetic(10_120, 16, "clusters", rng_seed=2)
+    _compare_grid(g, gi, V[10_000:10_048], "m", gold)
+
+
+def test_batch_shared_range_and_edges(g, golden):
+    gold = golden("small")
+    gi = g.load_index(gold["container"].tobytes(), g.BuildParams(k_max=16, k_local=8, bucket_capacity=250))
+    Q, _ = ist.gen_synthetic(64, 8, "clusters", rng_seed=1)
+    Q = Q + np.float32(0.01)
+    res = g.search_batch(gi, Q, g.SearchParams(k=10, range=g.RangePredicate(0.2, 0.45), itopk=64, rng_seed=21))
+    for i, r in enumerate(res):
+        c = gold["s_batch_counts"][i]
+        assert np.array_equal(r.slots, gold["s_batch_slots"][i, :c])
+    V, S = ist.gen_synthetic(2000, 8, "clusters", rng_seed=1)
+    srt = np.sort(S)
+    edges = [(2.0, 3.0), (float(srt[0]), float(srt[2])), (-np.inf, np.inf), (float(srt[0]), float(srt[-1]))]
+    for i, (lo, hi) in enumerate(edges):
+        r = g.search(gi, V[0], g.SearchParams(k=10, range=g.RangePredicate(lo, hi), itopk=64, rng_seed=5))
+        c = gold["edge_counts"][i]
+        assert np.array_equal(r.slots, gold["edge_slots"][i, :c])
+        assert r.truncated == bool(gold["edge_truncated"][i])
+
+
+def test_distance_soundness_is_bitwise(g, golden):
+    gold = golden("mid")
+    gi = g.load_index(gold["container"].tobytes())
+    V, S = ist.gen_synthetic(10_120, 16, "clusters", rng_seed=2)
+    Q = V[10_000:10_060]
+    ranges = beam.window_ranges(S[:10_000], 0.2, len(Q), 11)
+    X = gi.store.X
+    for i, (lo, hi) in enumerate(ranges):
+        r = g.search(gi, Q[i], g.SearchParams(k=10, range=g.RangePredicate(lo, hi), rng_seed=i))
+        s = gi.store.scalars[r.slots]
+        assert np.all((s >= np.float32(lo)) & (s <= np.float32(hi)))
+        for slot, d in zip(r.slots, r.sq_dists):
+            assert d == g.sq_distance(Q[i], X[slot])
+        assert r.stats.dist_evals == r.stats.seed_evals + r.stats.in_range_new
+
+
+def test_container_roundtrip_and_views(g, golden, tmp_path):
+    gold = golden("small")
+    raw = gold["container"].tobytes()
+    gi = g.load_index(raw, g.BuildParams(k_max=16, k_local=8, bucket_capacity=250))
+    p = tmp_path / "x.grab"
+    g.save_index(gi, p)
+    assert p.read_bytes() == raw
+    ref = ist.index_from_container(raw)
+    assert [len(x) for x in gi.meta.bucket_to_index] == [len(x) for x in ref.b2i]
+    assert gi.meta.bucket_to_index == ref.b2i
+
+
+def test_bucket_selection_bit_exact(g, golden):
+    gold = golden("layout")
+    meta = g.BucketMeta(boundaries=gold["iv_boundaries"], index_to_bucket=np.empty(0, np.int32),
+                        bucket_to_index=[])
+    for lo, hi, want in zip(gold["iv_lower"], gold["iv_upper"], gold["iv_lohi"]):
+        assert g.intersecting_buckets(meta, g.RangePredicate(float(lo), float(hi))) == tuple(want)
+    assert np.array_equal(g.bucket_ids_of(meta, gold["bid_scalars"]), gold["bid_ids"])
+
+
+def test_search_empty_index(g):
+    gi = g.create_index(4, 16, g.BuildParams(k_max=4, k_local=2))
+    r = g.search(gi, np.zeros(4, np.float32), g.SearchParams(k=3, itopk=8))
+    assert len(r) == 0 and not r.truncated
