@@ -115,6 +115,20 @@ GRAB_API int grab_sync(grab_index* h);
 GRAB_API int grab_build(grab_index* h, const float* vectors, const float* scalars, uint64_t n, int strategy,
                uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report);
 
+/* Optional capture of the intermediate graphs (host pointers, slot ids, NULL
+ * to skip): pass-1 forward kNN rows and merged rows (LocalGraphDraft,
+ * builder.py:38-52), necessary counts, and the pass-2 global rows
+ * (GlobalGraph.rows, builder.py:55-60), each [n x k] with k = k_max / k_g. */
+typedef struct {
+  uint32_t* forward_rows;
+  uint32_t* merged_rows;
+  uint32_t* necessary;
+  uint32_t* global_rows;
+} grab_build_debug;
+GRAB_API int grab_build_ex(grab_index* h, const float* vectors, const float* scalars, uint64_t n,
+                           int strategy, uint32_t k_g, uint32_t refine_rounds, uint32_t mem,
+                           grab_build_report* report, const grab_build_debug* debug);
+
 /* ---- insert_batch (updater.py:154-263) ---- */
 GRAB_API int grab_insert(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids,
                 uint64_t b, uint32_t search_itopk, uint32_t mem, grab_insert_report* report);

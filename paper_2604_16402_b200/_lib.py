@@ -52,6 +52,11 @@ INSERT_FIELDS = ["batch_size", "bulk_built", "forward_accepted", "forward_reject
                  "reverse_rejected", "evictions_necessary", "evictions_redundant", "forced_links", "n_rewired"]
 
 
+class BuildDebugC(C.Structure):
+    _fields_ = [("forward_rows", C.c_void_p), ("merged_rows", C.c_void_p), ("necessary", C.c_void_p),
+                ("global_rows", C.c_void_p)]
+
+
 class InsertReportC(C.Structure):
     _fields_ = [(f, C.c_uint64) for f in INSERT_FIELDS] + [("wall_time_s", C.c_double)]
 
@@ -72,6 +77,7 @@ _SIGS = {
     "grab_get_info": (C.c_int, [P, C.POINTER(InfoC)]),
     "grab_sync": (C.c_int, [P]),
     "grab_build": (C.c_int, [P, P, P, u64, C.c_int, u32, u32, u32, C.POINTER(BuildReportC)]),
+    "grab_build_ex": (C.c_int, [P, P, P, u64, C.c_int, u32, u32, u32, C.POINTER(BuildReportC), P]),
     "grab_insert": (C.c_int, [P, P, P, P, u64, u32, u32, C.POINTER(InsertReportC)]),
     "grab_last_rewired": (C.c_int, [P, P, u64, C.POINTER(u64)]),
     "grab_search": (C.c_int, [P, P, u64, P, P, u64, C.POINTER(SearchParamsC), P, u64, u64, u64, P, P, P, P, u32, P]),

@@ -246,3 +246,92 @@ def intersecting_buckets(meta, rng: RangePredicate) -> tuple[int, int]:
         bd = np.ascontiguousarray(meta.boundaries, dtype=np.float32)
         L.check(L.lib.grab_bucket_select_raw(L.ptr(bd), len(bd) - 1, L.ptr(lo), L.ptr(hi), 1, L.ptr(a), L.ptr(b)))
     return int(a[0]), int(b[0])
+
+
+# ---- build_index (builder.py:503-548) -----------------------------------------
+@dataclass
+class BuildReport:
+    """builder.py:63-76."""
+
+    n: int = 0
+    m: int = 0
+    phase1_seconds: float = 0.0
+    phase2_seconds: float = 0.0
+    fuse_seconds: float = 0.0
+    total_seconds: float = 0.0
+    bucket_sizes: list = field(default_factory=list)
+    isolated_nodes: int = 0
+    cross_bucket_edge_ratio: float = 0.0
+
+    def to_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+@dataclass
+class BuildDraft:
+    """Intermediate graphs of a build (LocalGraphDraft + GlobalGraph rows, slot ids)."""
+
+    forward_rows: np.ndarray
+    rows: np.ndarray
+    necessary_counts: np.ndarray
+    global_rows: np.ndarray
+
+
+_STRATEGY = {"quantile": 0, "width": 1}
+
+
+def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None = None, headroom: float = 2.0,
+                bucket_strategy: str = "quantile", n_threads: int = 1, k_g: int | None = None,
+                refine_rounds: int = 3, device: int = 0, return_draft: bool = False):
+    """Full static build on the device: partition, slab layout, pass 1, pass 2, fuse, repair.
+
+    Returns (GraphIndex, BuildReport) like the reference, plus a BuildDraft when
+    ``return_draft``. ``n_threads`` is accepted for signature parity (the GPU is
+    the parallelism).
+    """
+    del n_threads
+    if bucket_strategy not in _STRATEGY:
+        raise ValueError(f"unknown bucket strategy: {bucket_strategy!r}")
+    dev = _is_dev(vectors)
+    if dev:
+        V = vectors.contiguous()
+        S = scalars.contiguous()
+        n, dim = V.shape
+        mem = L.MEM_DEVICE
+    else:
+        V = np.ascontiguousarray(vectors, dtype=np.float32)
+        S = np.ascontiguousarray(scalars, dtype=np.float32)
+        if V.ndim != 2:
+            raise DimensionMismatchError(f"vectors must be 2-D, got {V.shape}")
+        n, dim = V.shape
+        if len(S) != n:
+            raise ValueError(f"{n} vectors but {len(S)} scalars")
+        if not np.all(np.isfinite(S)):
+            raise ValueError("scalars must be finite")
+        mem = L.MEM_HOST
+    if capacity is None:
+        capacity = max(int(n * headroom), n)
+    index = create_index(dim, capacity, params, device)
+    kg = params.k_max if k_g is None else int(k_g)
+    rep = L.BuildReportC()
+    dbg = None
+    draft = None
+    if return_draft:
+        draft = BuildDraft(np.empty((n, params.k_max), "<u4"), np.empty((n, params.k_max), "<u4"),
+                           np.empty(n, "<u4"), np.empty((n, kg), "<u4"))
+        dbg = L.BuildDebugC(L.ptr(draft.forward_rows), L.ptr(draft.rows), L.ptr(draft.necessary_counts),
+                            L.ptr(draft.global_rows))
+    L.check(L.lib.grab_build_ex(index.handle, L.ptr(V), L.ptr(S), n, _STRATEGY[bucket_strategy], kg,
+                                refine_rounds, mem, C.byref(rep), C.byref(dbg) if dbg is not None else None))
+    index._ids[:n] = np.arange(n)
+    index._touch()
+    meta = index.meta
+    report = BuildReport(n=int(rep.n), m=int(rep.m), phase1_seconds=rep.phase1_seconds,
+                         phase2_seconds=rep.phase2_seconds, fuse_seconds=rep.fuse_seconds,
+                         total_seconds=rep.total_seconds,
+                         bucket_sizes=[len(b) for b in meta.bucket_to_index] if meta else [],
+                         isolated_nodes=int(rep.isolated_nodes),
+                         cross_bucket_edge_ratio=float(rep.cross_bucket_edge_ratio))
+    if return_draft:
+        return index, report, draft
+    return index, report

@@ -428,6 +428,18 @@ extern "C" int grab_build(grab_index* h, const float* vectors, const float* scal
   });
 }
 
+extern "C" int grab_build_ex(grab_index* h, const float* vectors, const float* scalars, uint64_t n, int strategy,
+                             uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report,
+                             const grab_build_debug* debug) {
+  return guarded([&] {
+    check_handle(h);
+    std::lock_guard<std::mutex> lk(h->writer);
+    DevIndex& ix = h->ix;
+    set_device(ix);
+    build_index_device(ix, vectors, scalars, n, strategy, k_g, refine_rounds, mem, report, debug);
+  });
+}
+
 extern "C" int grab_insert(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
                            uint32_t search_itopk, uint32_t mem, grab_insert_report* report) {
   return guarded([&] {

@@ -1,0 +1,24 @@
+// kNN engine shared by pass 1 (per-bucket slabs), pass 2 (global) and insert
+// candidate generation: screen + exact f64 rerank.
+#pragma once
+#include <vector>
+
+#include "index.cuh"
+
+namespace grab {
+
+constexpr uint32_t kKnnBM = 128;  // query rows per job / CTA
+
+// rows [r0, r0+nr) (phys) against candidate phys range [c0, c1)
+struct KnnJob {
+  uint32_t r0, nr, c0, c1;
+};
+
+// For every query row p of every job: out_ids[p*K + j] / out_d[p*K + j] = the
+// K nearest valid candidates (excluding p itself), ascending by (f64 dist,
+// tiebreak) where tiebreak = slot (tb_slot) or phys (slab-local column order).
+// Unfilled entries stay as initialised by the caller (SENTINEL).
+void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob>& jobs, uint32_t K, bool tb_slot,
+                uint32_t* out_ids, double* out_d, cudaStream_t st);
+
+}  // namespace grab

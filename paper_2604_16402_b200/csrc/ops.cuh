@@ -11,7 +11,8 @@ void run_bruteforce(const DevIndex& ix, const float* Q, uint64_t nq, const doubl
 void run_sq_distances(const float* q, const float* rows, uint64_t n, uint32_t dp, double* out, cudaStream_t st);
 // build.cu
 void build_index_device(DevIndex& ix, const float* vectors, const float* scalars, uint64_t n, int strategy,
-                        uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report);
+                        uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report,
+                        const grab_build_debug* dbg = nullptr);
 // insert.cu
 void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
                          uint32_t search_itopk, uint32_t mem, grab_insert_report* report);
