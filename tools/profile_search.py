@@ -1,0 +1,35 @@
+"""Build a config on the GPU and run the search kernel a few times (for ncu).
+
+    ncu --set full -k regex:k_search -s 2 -c 1 -o gpurun_out/search python tools/profile_search.py --config cfg2
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2604_16402_b200 as g  # noqa: E402
+from paper_2604_16402_b200 import datasets as ds  # noqa: E402
+
+P = {"cfg1": (100_000, 128, 6250, 1000, 96, 4, 50), "cfg2": (1_000_000, 128, 10_000, 10_000, 256, 4, 100)}
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--itopk", type=int)
+ap.add_argument("--width", type=int)
+ap.add_argument("--iters", type=int)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+n, dim, cap, nq, itopk, width, iters = P[a.config]
+itopk = a.itopk or itopk
+width = a.width or width
+iters = a.iters or iters
+X, S = ds.gen_lowrank(n, dim, seed=0)
+Q = ds.lowrank_queries(nq, dim, seed=1)
+lo, hi = ds.range_arrays(ds.generate_ranges(S, 0.1, nq, 0))
+gi, rep = g.build_index(X, S, g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap))
+sp = g.SearchParams(k=10, itopk=itopk, search_width=width, max_iterations=iters)
+for _ in range(a.reps):
+    r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0)
+st = r.stats
+print("mean stats:", {f: float(np.mean(st[f])) for f in st.dtype.names})
