@@ -7,13 +7,15 @@ importing without the built library raises ImportError.
 from .params import (BuildParams, CapacityError, DimensionMismatchError, RangePredicate, SearchParams,
                      VectorRecord)
 from .graph import SENTINEL, BucketMeta, GraphIndex, create_index, from_reference, load_index, save_index
-from .api import (BatchResult, BuildDraft, BuildReport, build_index, SearchResult, SearchStats, brute_force_arrays, brute_force_search, bucket_ids_of,
+from .api import (BatchResult, BuildDraft, BuildReport, InsertReport, build_index, insert_batch, select_neighbors,
+                  try_rewire, SearchResult, SearchStats, brute_force_arrays, brute_force_search, bucket_ids_of,
                   bucket_of, intersecting_buckets, search, search_arrays, search_batch, sq_distance, sq_distances)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchResult", "BuildDraft", "BuildReport", "build_index", "BucketMeta", "BuildParams", "CapacityError", "DimensionMismatchError", "GraphIndex",
+    "BatchResult", "BuildDraft", "BuildReport", "InsertReport", "build_index", "insert_batch", "select_neighbors",
+    "try_rewire", "BucketMeta", "BuildParams", "CapacityError", "DimensionMismatchError", "GraphIndex",
     "RangePredicate", "SENTINEL", "SearchParams", "SearchResult", "SearchStats", "VectorRecord",
     "brute_force_arrays", "brute_force_search", "bucket_ids_of", "bucket_of", "create_index", "from_reference",
     "intersecting_buckets", "load_index", "save_index", "search", "search_arrays", "search_batch",

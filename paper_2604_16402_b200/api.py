@@ -335,3 +335,105 @@ def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None =
     if return_draft:
         return index, report, draft
     return index, report
+
+
+# ---- insert_batch (updater.py:154-263) ----------------------------------------
+@dataclass
+class InsertReport:
+    """updater.py:31-46."""
+
+    batch_size: int = 0
+    bulk_built: int = 0
+    forward_accepted: int = 0
+    forward_rejected: int = 0
+    reverse_accepted: int = 0
+    reverse_rejected: int = 0
+    evictions_necessary: int = 0
+    evictions_redundant: int = 0
+    forced_links: int = 0
+    rewired_rows: list = field(default_factory=list)
+    wall_time_s: float = 0.0
+
+    def to_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk: int = 128) -> InsertReport:
+    """Integrate one batch on the device: append, candidates, forward pruning, reverse rewiring, healing."""
+    dev = _is_dev(vectors)
+    if dev:
+        V = vectors.contiguous()
+        S = scalars.contiguous()
+        b = V.shape[0]
+        mem = L.MEM_DEVICE
+        Ih = None if ids is None else np.ascontiguousarray(ids.cpu().numpy() if hasattr(ids, "cpu") else ids,
+                                                           dtype=np.int64)
+    else:
+        V = np.asarray(vectors, dtype=np.float32)
+        S = np.ascontiguousarray(np.asarray(scalars, dtype=np.float32).reshape(-1))
+        b = len(V)
+        mem = L.MEM_HOST
+        Ih = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+    if b == 0:
+        return InsertReport(batch_size=0)
+    if V.ndim != 2 or V.shape[1] != index.dim:
+        raise DimensionMismatchError(f"vectors have shape {tuple(V.shape)}, index dimension is {index.dim}")
+    if len(S) != b:
+        raise ValueError(f"{b} vectors but {len(S)} scalars")
+    if not dev:
+        V = np.ascontiguousarray(V)
+        if not np.all(np.isfinite(S)):
+            raise ValueError("scalars must be finite")
+    rep = L.InsertReportC()
+    L.check(L.lib.grab_insert(index.handle, L.ptr(V), L.ptr(S), L.ptr(Ih), b, int(search_itopk), mem,
+                              C.byref(rep)))
+    index._touch()
+    n0 = index.count - b
+    if Ih is not None:
+        index._ids[n0:n0 + b] = Ih
+    else:
+        index._ids[n0:n0 + b] = np.arange(n0, n0 + b)
+    rw = np.empty(int(rep.n_rewired), dtype=np.uint32)
+    nout = C.c_uint64()
+    if len(rw):
+        L.check(L.lib.grab_last_rewired(index.handle, L.ptr(rw), len(rw), C.byref(nout)))
+    return InsertReport(batch_size=int(rep.batch_size), bulk_built=int(rep.bulk_built),
+                        forward_accepted=int(rep.forward_accepted), forward_rejected=int(rep.forward_rejected),
+                        reverse_accepted=int(rep.reverse_accepted), reverse_rejected=int(rep.reverse_rejected),
+                        evictions_necessary=int(rep.evictions_necessary),
+                        evictions_redundant=int(rep.evictions_redundant), forced_links=int(rep.forced_links),
+                        rewired_rows=[int(x) for x in rw], wall_time_s=float(rep.wall_time_s))
+
+
+def _rows_of(store) -> np.ndarray:
+    X = store.X if hasattr(store, "X") else store
+    return np.ascontiguousarray(X, dtype=np.float32)
+
+
+def select_neighbors(store, target: int, candidates, row_capacity: int, alpha: float, fresh) -> list[int]:
+    """updater.py:49-84 on the device (Eq.1 with the Eq.2 alpha^2 bias on fresh candidates)."""
+    if not candidates:
+        return []
+    X = _rows_of(store)
+    cs = np.ascontiguousarray([int(c[0]) for c in candidates], dtype=np.int64)
+    cd = np.ascontiguousarray([float(c[1]) for c in candidates], dtype=np.float64)
+    fr = np.ascontiguousarray([1 if int(c[0]) in fresh else 0 for c in candidates], dtype=np.uint8)
+    out = np.empty(max(int(row_capacity), 1), dtype=np.int64)
+    n = C.c_uint32()
+    L.check(L.lib.grab_select_neighbors(L.ptr(X), X.shape[0], X.shape[1], int(target), L.ptr(cs), L.ptr(cd),
+                                        L.ptr(fr), len(cs), int(row_capacity), float(alpha), L.ptr(out),
+                                        C.byref(n)))
+    return [int(x) for x in out[: n.value]]
+
+
+def try_rewire(store, adjacency: np.ndarray, v: int, q: int, sq_dvq: float, alpha: float,
+               k_local: int) -> tuple[bool, int]:
+    """updater.py:87-123 on the device; mutates ``adjacency[v]`` in place like the reference."""
+    X = _rows_of(store)
+    row = np.ascontiguousarray(adjacency[v], dtype=np.uint32)
+    acc = C.c_int32()
+    pos = C.c_int32()
+    L.check(L.lib.grab_try_rewire(L.ptr(X), X.shape[0], X.shape[1], L.ptr(row), len(row), int(v), int(q),
+                                  float(sq_dvq), float(alpha), int(k_local), C.byref(acc), C.byref(pos)))
+    adjacency[v] = row
+    return bool(acc.value), int(pos.value)

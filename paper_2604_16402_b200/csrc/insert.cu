@@ -1,16 +1,797 @@
-// placeholder until the insert pipeline lands
+// Append-only batched insertion (reference updater.py:154-263).
+//
+//   append            append_batch (layout.py:181-223): tail claim, bucket ids,
+//                     zero-shift slab placement (relayout only on slab overflow)
+//   candidates        _bucket_candidates (updater.py:126-151): exact in-bucket
+//                     top-2*K_max among members with slot < q (causal kNN on the
+//                     slab), plus a full-range beam search (itopk = k = 128,
+//                     width 4, 50 iterations, live_count = n0, seed =
+//                     derive_query_seed(rng_seed, q)) for every fresh q at once
+//   forward           union, (dist, slot) order, nearest pre-batch node,
+//                     select_neighbors (updater.py:49-84), intra-then-cross row
+//   reverse           requests sorted by (v, q); one warp per target v applies
+//                     try_rewire (updater.py:87-123) serially, targets in parallel
+//   heal              _heal_unreachable (updater.py:266-324), sequential warp
+//
+// The forward stage only reads rows < n0 and writes fresh rows, so it runs for
+// the whole batch in parallel without changing the result.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "index.cuh"
+#include "knn.cuh"
 #include "ops.cuh"
+#include "search.cuh"
+
 namespace grab {
-void insert_batch_device(DevIndex&, const float*, const float*, const int64_t*, uint64_t, uint32_t, uint32_t,
-                         grab_insert_report*) {
-  throw Error(GRAB_ERR_STATE, "insert not implemented yet");
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
-void select_neighbors_device(const float*, uint64_t, uint32_t, int64_t, const int64_t*, const double*, const uint8_t*,
-                             uint32_t, uint32_t, double, int64_t*, uint32_t*) {
-  throw Error(GRAB_ERR_STATE, "nyi");
+
+struct Pool {
+  std::vector<void*> ptrs;
+  cudaStream_t st;
+  explicit Pool(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    GRAB_CUDA(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  ~Pool() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+// ------------------------------------------------------------- warp distance
+template <int NC>
+struct RowRegs {
+  float4 v[NC];
+};
+
+template <int NC>
+__device__ __forceinline__ void load_row(RowRegs<NC>& r, const float* X, uint32_t dp, uint32_t p) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    uint32_t col = (c * 32 + lane_id()) * 4;
+    r.v[c] = col < dp ? *reinterpret_cast<const float4*>(X + (uint64_t)p * dp + col) : make_float4(0, 0, 0, 0);
+  }
 }
-void try_rewire_device(const float*, uint64_t, uint32_t, uint32_t*, uint32_t, uint32_t, uint32_t, double, double,
-                       uint32_t, int32_t*, int32_t*) {
-  throw Error(GRAB_ERR_STATE, "nyi");
+
+template <int NC>
+__device__ __forceinline__ double row_dist(const RowRegs<NC>& q, const float* X, uint32_t dp, uint32_t p) {
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    uint32_t col = (c * 32 + lane_id()) * 4;
+    if (col < dp) acc = sq4(ldg_nc_f4(X + (uint64_t)p * dp + col), q.v[c], acc);
+  }
+  return warp_sum(acc);
 }
+
+// ------------------------------------------------------------- shared counters
+struct InsertCounters {
+  unsigned long long forward_accepted, forward_rejected, reverse_accepted, reverse_rejected;
+  unsigned long long evictions_necessary, evictions_redundant, forced_links, n_requests;
+};
+
+// ------------------------------------------------------------- forward stage
+// Warp per fresh node (slot start + i): union of in-bucket candidates (phys,
+// f64) and search results (slot, f64) -> sort by (dist, slot) -> dedup ->
+// nearest pre-batch -> greedy Eq.1/Eq.2 selection -> forward row + requests.
+template <int NC>
+__global__ void k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const Attr* attr, const int32_t* i2b,
+                          const float* X, uint32_t dp, uint32_t* adj, uint32_t K, const uint32_t* loc_ids,
+                          const double* loc_d, uint32_t KL, const int64_t* found_slots, const double* found_d,
+                          const uint32_t* found_cnt, uint32_t KS, double alpha2, uint32_t P,
+                          unsigned long long* req_key, double* req_d, uint32_t* nearest_pre, InsertCounters* cnt) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t wib = threadIdx.x >> 5, lane = lane_id(), wpb = blockDim.x >> 5;
+  const uint64_t i = blockIdx.x * (uint64_t)wpb + wib;
+  if (i >= b) return;
+  double* cd = (double*)smem + (uint64_t)wib * P;
+  double* near = (double*)smem + (uint64_t)wpb * P + (uint64_t)wib * P;
+  double* acc_d = (double*)smem + 2ull * wpb * P + (uint64_t)wib * K;                 // accepted dists (K)
+  uint32_t* cs = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wib * P;  // slot
+  uint32_t* acc_s = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wpb * P +
+                    (uint64_t)wib * K;  // accepted slots (K)
+  const uint64_t q = start + i;
+  const uint32_t pq = s2p[q];
+  // gather candidates
+  uint32_t n = 0;
+  for (uint32_t j = lane; j < P; j += 32) {
+    cd[j] = __longlong_as_double(0x7FF0000000000000ll);
+    cs[j] = kSentinel;
+  }
+  __syncwarp();
+  for (uint32_t j = lane; j < KL; j += 32) {
+    uint32_t c = loc_ids[(uint64_t)pq * KL + j];
+    if (c != kSentinel) {
+      cd[j] = loc_d[(uint64_t)pq * KL + j];
+      cs[j] = attr[c].slot;
+    }
+  }
+  const uint32_t nf = found_cnt ? found_cnt[i] : 0;
+  for (uint32_t j = lane; j < nf; j += 32) {
+    cd[KL + j] = found_d[i * KS + j];
+    cs[KL + j] = (uint32_t)found_slots[i * KS + j];
+  }
+  __syncwarp();
+  // bitonic sort by (dist, slot)
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = lane; t < P; t += 32) {
+        uint32_t l = t ^ j;
+        if (l > t) {
+          bool asc = (t & k) == 0;
+          bool gt = key_less(cd[l], cs[l], cd[t], cs[t]);
+          if (gt == asc) {
+            double td = cd[t];
+            cd[t] = cd[l];
+            cd[l] = td;
+            uint32_t ts = cs[t];
+            cs[t] = cs[l];
+            cs[l] = ts;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // dedup (a slot found by both sources carries identical f64 distance bits):
+  // flags from the unmodified array first, then an order-preserving compaction
+  uint32_t keep_bits = 0;
+  for (uint32_t c = 0; c * 32 < P; ++c) {
+    uint32_t t = c * 32 + lane;
+    if (cs[t] != kSentinel && (t == 0 || cs[t] != cs[t - 1])) keep_bits |= 1u << c;
+  }
+  __syncwarp();
+  for (uint32_t c = 0; c * 32 < P; ++c) {
+    uint32_t t = c * 32 + lane;
+    bool keep = (keep_bits >> c) & 1u;
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
+    double dv = cd[t];
+    uint32_t sv = cs[t];
+    __syncwarp();
+    if (keep) {
+      uint32_t pos = n + __popc(m & ((1u << lane) - 1));
+      cd[pos] = dv;
+      cs[pos] = sv;
+    }
+    n += __popc(m);
+    __syncwarp();
+  }
+  if (n == 0) {
+    if (lane == 0) nearest_pre[i] = kSentinel;
+    return;
+  }
+  // nearest pre-batch node (updater.py:225-228)
+  uint32_t npre = kSentinel;
+  for (uint32_t t0 = 0; t0 < n && npre == kSentinel; t0 += 32) {
+    uint32_t t = t0 + lane;
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, t < n && cs[t] < start);
+    if (m) npre = cs[t0 + __ffs(m) - 1];
+  }
+  if (lane == 0) nearest_pre[i] = npre;
+  // greedy selection (select_neighbors)
+  for (uint32_t t = lane; t < n; t += 32) near[t] = __longlong_as_double(0x7FF0000000000000ll);
+  __syncwarp();
+  uint32_t nacc = 0;
+  for (uint32_t t = 0; t < n && nacc < K; ++t) {
+    const uint32_t s = cs[t];
+    if (s == (uint32_t)q) continue;
+    const double d = cd[t];
+    const double de = s >= start ? alpha2 * d : d;
+    if (!(de < near[t])) continue;
+    if (lane == 0) {
+      acc_s[nacc] = s;
+      acc_d[nacc] = d;
+    }
+    ++nacc;
+    // nearest_kept[j] = min(nearest_kept[j], dist(s, cand j)) for the undecided tail
+    RowRegs<NC> r;
+    load_row<NC>(r, X, dp, s2p[s]);
+    for (uint32_t j = t + 1; j < n; ++j) {
+      double dj = row_dist<NC>(r, X, dp, s2p[cs[j]]);
+      if (lane == 0 && dj < near[j]) near[j] = dj;
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    atomicAdd(&cnt->forward_accepted, (unsigned long long)nacc);
+    atomicAdd(&cnt->forward_rejected, (unsigned long long)(n - nacc));
+  }
+  // forward row: intra-bucket accepts first, then cross (updater.py:236-240)
+  const int32_t bq = i2b[q];
+  uint32_t* row = adj + (uint64_t)pq * K;
+  if (lane == 0) {
+    uint32_t col = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (uint32_t j = 0; j < nacc; ++j) {
+        uint32_t s = acc_s[j];
+        bool intra = i2b[s] == bq;
+        if ((pass == 0) == intra) {
+          row[col] = s2p[s];
+          // reverse request (v, q, d_vq) with the candidate distance
+          req_key[i * K + col] = ((unsigned long long)s << 32) | (unsigned long long)q;
+          req_d[i * K + col] = acc_d[j];
+          ++col;
+        }
+      }
+  }
+}
+
+// ------------------------------------------------------------- reverse stage
+__global__ void k_req_heads(const unsigned long long* keys, uint64_t n, uint8_t* head) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+}
+
+// try_rewire for every request of one target v, in q order (updater.py:87-123)
+template <int NC>
+__global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint64_t nreq, const uint32_t* heads,
+                         uint32_t nheads, const uint32_t* s2p, const Attr* attr, const float* X, uint32_t dp,
+                         uint32_t* adj, uint32_t K, uint32_t k_local, double alpha2, uint8_t* rewired_slot,
+                         InsertCounters* cnt) {
+  const uint32_t wib = threadIdx.x >> 5, lane = lane_id(), wpb = blockDim.x >> 5;
+  const uint64_t h = blockIdx.x * (uint64_t)wpb + wib;
+  if (h >= nheads) return;
+  const uint64_t b0 = heads[h], b1 = h + 1 < nheads ? heads[h + 1] : nreq;
+  const uint32_t v = (uint32_t)(keys[b0] >> 32);
+  const uint32_t pv = s2p[v];
+  uint32_t* row = adj + (uint64_t)pv * K;
+  unsigned long long acc = 0, rej = 0, ev_nec = 0, ev_red = 0;
+  RowRegs<NC> rv;
+  load_row<NC>(rv, X, dp, pv);
+  for (uint64_t r = b0; r < b1; ++r) {
+    const uint32_t q = (uint32_t)keys[r];
+    const uint32_t pq = s2p[q];
+    // duplicate?
+    bool dup = false, has_free = false;
+    int32_t free_pos = -1;
+    for (uint32_t c0 = 0; c0 < K; c0 += 32) {
+      uint32_t c = c0 + lane;
+      uint32_t e = c < K ? row[c] : 0u;
+      dup |= __any_sync(0xFFFFFFFFu, c < K && e == pq);
+      uint32_t fm = __ballot_sync(0xFFFFFFFFu, c < K && e == kSentinel);
+      if (fm && !has_free) {
+        has_free = true;
+        free_pos = (int32_t)(c0 + __ffs(fm) - 1);
+      }
+    }
+    if (dup) {
+      ++rej;
+      continue;
+    }
+    if (has_free) {
+      __syncwarp();
+      if (lane == 0) row[free_pos] = pq;
+      __syncwarp();
+      ++acc;
+      continue;
+    }
+    // Eq.1/Eq.2 test against every current neighbour
+    const double deff = alpha2 * dvq[r];
+    RowRegs<NC> rq;
+    load_row<NC>(rq, X, dp, pq);
+    bool ok = true;
+    for (uint32_t j = 0; j < K && ok; ++j) ok = deff < row_dist<NC>(rq, X, dp, row[j]);
+    if (!ok) {
+      ++rej;
+      continue;
+    }
+    const uint32_t r0 = K > k_local ? k_local : 0;
+    double best = -1.0;
+    int32_t pos = -1;
+    for (uint32_t j = r0; j < K; ++j) {
+      double dj = row_dist<NC>(rv, X, dp, row[j]);
+      if (dj > best) {
+        best = dj;
+        pos = (int32_t)j;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) row[pos] = pq;
+    __syncwarp();
+    ++acc;
+    if ((uint32_t)pos >= k_local)
+      ++ev_red;
+    else
+      ++ev_nec;
+  }
+  if (lane == 0) {
+    atomicAdd(&cnt->reverse_accepted, acc);
+    atomicAdd(&cnt->reverse_rejected, rej);
+    atomicAdd(&cnt->evictions_necessary, ev_nec);
+    atomicAdd(&cnt->evictions_redundant, ev_red);
+    if (acc) rewired_slot[v] = 1;
+  }
+}
+
+// ------------------------------------------------------------- heal stage
+__global__ void k_prefix_indeg(const uint32_t* adj, const uint32_t* s2p, const Attr* attr, uint64_t prefix,
+                               uint32_t K, uint64_t start, uint64_t end, uint32_t* counts) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= prefix * K) return;
+  uint32_t v = adj[(uint64_t)s2p[i / K] * K + i % K];
+  if (v == kSentinel) return;
+  uint32_t s = attr[v].slot;
+  if (s >= start && s < end) atomicAdd(counts + (s - start), 1u);
+}
+
+template <int NC>
+__global__ void k_heal(const uint32_t* missing, uint32_t nmiss, uint64_t start, uint64_t end, const uint32_t* s2p,
+                       const Attr* attr, const float* X, uint32_t dp, uint32_t* adj, uint32_t K, uint32_t k_local,
+                       const uint32_t* nearest_pre, uint8_t* rewired_slot, InsertCounters* cnt) {
+  const uint32_t lane = lane_id();
+  for (uint32_t t = 0; t < nmiss; ++t) {
+    const uint64_t q = start + missing[t];
+    const uint32_t pq = s2p[q];
+    const uint32_t* rq = adj + (uint64_t)pq * K;
+    RowRegs<NC> qr;
+    load_row<NC>(qr, X, dp, pq);
+    // nearest pre-batch entry of q's own row, ties by slot
+    double bd = __longlong_as_double(0x7FF0000000000000ll);
+    uint32_t v = kSentinel;
+    for (uint32_t j = 0; j < K; ++j) {
+      uint32_t e = rq[j];
+      if (e == kSentinel) continue;
+      uint32_t s = attr[e].slot;
+      if (s >= start) continue;
+      double d = row_dist<NC>(qr, X, dp, e);
+      if (key_less(d, s, bd, v)) {
+        bd = d;
+        v = s;
+      }
+    }
+    if (v == kSentinel) v = nearest_pre[missing[t]];
+    if (v == kSentinel) continue;
+    const uint32_t pv = s2p[v];
+    uint32_t* row = adj + (uint64_t)pv * K;
+    int32_t free_pos = -1;
+    for (uint32_t j = 0; j < K; ++j)
+      if (row[j] == kSentinel) {
+        free_pos = (int32_t)j;
+        break;
+      }
+    if (free_pos >= 0) {
+      __syncwarp();
+      if (lane == 0) row[free_pos] = pq;
+    } else {
+      const uint32_t r0 = K > k_local ? k_local : 0;
+      RowRegs<NC> vr;
+      load_row<NC>(vr, X, dp, pv);
+      double best_st = -1.0, best_any = -1.0;
+      int32_t pos_st = -1, pos_any = -1;
+      for (uint32_t j = r0; j < K; ++j) {
+        uint32_t e = row[j];
+        double d = row_dist<NC>(vr, X, dp, e);
+        uint32_t s = attr[e].slot;
+        if (d > best_any) {
+          best_any = d;
+          pos_any = (int32_t)j;
+        }
+        if ((s < start || s >= end) && d > best_st) {
+          best_st = d;
+          pos_st = (int32_t)j;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) row[pos_st >= 0 ? pos_st : pos_any] = pq;
+      if (lane == 0) cnt->evictions_redundant += 1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      cnt->forced_links += 1;
+      rewired_slot[v] = 1;
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------- driver
+template <class F>
+static void by_nc(uint32_t dp, F&& f) {
+  uint32_t nc = (uint32_t)div_up(dp, 128);
+  if (nc <= 1)
+    f(std::integral_constant<int, 1>{});
+  else if (nc <= 2)
+    f(std::integral_constant<int, 2>{});
+  else if (nc <= 4)
+    f(std::integral_constant<int, 4>{});
+  else if (nc <= 8)
+    f(std::integral_constant<int, 8>{});
+  else
+    throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported");
+}
+
+__global__ void k_fresh_phys(const uint32_t* s2p, uint64_t start, uint64_t b, uint32_t* out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < b) out[i] = s2p[start + i];
+}
+
+void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
+                         uint32_t search_itopk, uint32_t mem, grab_insert_report* rep) {
+  const double t_begin = now_s();
+  cudaStream_t st = ix.stream;
+  grab_insert_report R{};
+  R.batch_size = b;
+  ix.last_rewired.clear();
+  Pool pool(st);
+  // stage rows on the device
+  const float* Vd = vectors;
+  const float* Sd = scalars;
+  if (b && mem == GRAB_MEM_HOST) {
+    for (uint64_t i = 0; i < b; ++i)
+      if (!std::isfinite(scalars[i])) throw Error(GRAB_ERR_VALUE, "scalars must be finite");
+    float* v = pool.alloc<float>(b * ix.dim);
+    float* s = pool.alloc<float>(b);
+    GRAB_CUDA(cudaMemcpyAsync(v, vectors, b * ix.dim * 4, cudaMemcpyHostToDevice, st));
+    GRAB_CUDA(cudaMemcpyAsync(s, scalars, b * 4, cudaMemcpyHostToDevice, st));
+    Vd = v;
+    Sd = s;
+  }
+  // empty index: bulk-build the first bucket_capacity rows (updater.py:175-189)
+  if (ix.count == 0) {
+    if (b == 0) {
+      if (rep) *rep = R;
+      return;
+    }
+    uint64_t head = std::min<uint64_t>(b, ix.params.bucket_capacity);
+    build_index_device(ix, Vd, Sd, head, GRAB_STRATEGY_QUANTILE, ix.params.k_max, 3, GRAB_MEM_DEVICE, nullptr);
+    if (ids)
+      for (uint64_t i = 0; i < head; ++i) ix.ids[i] = ids[i];
+    R.bulk_built = head;
+    if (head == b) {
+      R.wall_time_s = now_s() - t_begin;
+      if (rep) *rep = R;
+      return;
+    }
+    Vd += head * ix.dim;
+    Sd += head;
+    if (ids) ids += head;
+    b -= head;
+  }
+  if (b == 0) {
+    R.wall_time_s = now_s() - t_begin;
+    if (rep) *rep = R;
+    return;
+  }
+  if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no bucket metadata");
+  const uint64_t n0 = ix.count;
+  if (n0 + b > ix.n_cap)
+    throw Error(GRAB_ERR_CAPACITY, "capacity exhausted: " + std::to_string(n0) + " claimed + " + std::to_string(b) +
+                                       " requested > " + std::to_string(ix.n_cap));
+  const uint64_t start = n0, end = n0 + b;
+  const uint32_t K = ix.params.k_max;
+  // ---- append (bucket ids, zero-shift placement)
+  launch_bucket_ids(ix, Sd, b, ix.i2b + start, st);
+  std::vector<uint32_t> old_count = ix.h_bcount;
+  layout_append(ix, Vd, Sd, start, b);
+  for (uint64_t i = 0; i < b; ++i) ix.ids[start + i] = ids ? ids[i] : (int64_t)(start + i);
+
+  // ---- in-bucket candidates: causal kNN over each touched slab
+  const uint32_t KL = 2 * K;
+  uint32_t* loc_ids = pool.alloc<uint32_t>(ix.phys_cap * (uint64_t)KL);
+  double* loc_d = pool.alloc<double>(ix.phys_cap * (uint64_t)KL);
+  GRAB_CUDA(cudaMemsetAsync(loc_ids, 0xFF, ix.phys_cap * (uint64_t)KL * 4, st));
+  {
+    float* norms = pool.alloc<float>(ix.phys_cap);
+    row_norms(ix, norms, st);
+    std::vector<KnnJob> jobs;
+    for (uint32_t k = 0; k < ix.m; ++k) {
+      uint32_t s0 = ix.h_bstart[k], c_old = old_count[k], c_new = ix.h_bcount[k];
+      for (uint32_t r = c_old; r < c_new; r += kKnnBM)
+        jobs.push_back({s0 + r, std::min<uint32_t>(kKnnBM, c_new - r), s0, s0 + c_new});
+    }
+    knn_device(ix, norms, jobs, KL, /*tb_slot=*/false, loc_ids, loc_d, st, /*causal=*/true);
+  }
+  // ---- full-range graph search over the pre-batch prefix
+  const uint32_t KS = search_itopk;
+  int64_t* found_slots = nullptr;
+  double* found_d = nullptr;
+  uint32_t* found_cnt = nullptr;
+  uint32_t* fresh_phys = pool.alloc<uint32_t>(b);
+  k_fresh_phys<<<(unsigned)div_up(b, 256), 256, 0, st>>>(ix.slot2phys, start, b, fresh_phys);
+  GRAB_CHECK_LAUNCH();
+  if (n0 > 0) {
+    found_slots = pool.alloc<int64_t>(b * KS);
+    found_d = pool.alloc<double>(b * KS);
+    found_cnt = pool.alloc<uint32_t>(b);
+    double* lo = pool.alloc<double>(1);
+    double* hi = pool.alloc<double>(1);
+    const double inf = INFINITY, ninf = -INFINITY;
+    GRAB_CUDA(cudaMemcpyAsync(lo, &ninf, 8, cudaMemcpyHostToDevice, st));
+    GRAB_CUDA(cudaMemcpyAsync(hi, &inf, 8, cudaMemcpyHostToDevice, st));
+    SearchArgs a{};
+    a.X = ix.X;
+    a.attr = ix.attr;
+    a.adj = ix.adj;
+    a.dp = ix.dp;
+    a.k_max = K;
+    a.bound = ix.bound;
+    a.m = ix.m;
+    a.bstart = ix.bstart;
+    a.bcount = ix.bcount;
+    a.bcum = ix.bcum;
+    a.n_live = n0;
+    a.Q = nullptr;
+    a.qphys = fresh_phys;
+    a.lower = lo;
+    a.upper = hi;
+    a.range_stride = 0;
+    a.seeds = nullptr;
+    a.seed_base = ix.params.rng_seed;
+    a.ordinal0 = start;
+    a.k = KS;
+    a.itopk = KS;
+    a.width = 4;
+    a.max_iter = 50;
+    a.want = std::min<uint32_t>(KS, 32);
+    a.nwork = (uint32_t)b;
+    a.out_slots = found_slots;
+    a.out_dists = found_d;
+    a.out_counts = found_cnt;
+    a.out_stats = nullptr;
+    run_search(ix, a, st);
+  }
+  // ---- forward selection
+  const double alpha2 = ix.params.alpha * ix.params.alpha;
+  InsertCounters* cnt = pool.alloc<InsertCounters>(1);
+  GRAB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(InsertCounters), st));
+  unsigned long long* req_key = pool.alloc<unsigned long long>(b * K);
+  double* req_d = pool.alloc<double>(b * K);
+  GRAB_CUDA(cudaMemsetAsync(req_key, 0xFF, b * K * 8, st));
+  uint32_t* nearest_pre = pool.alloc<uint32_t>(b);
+  uint32_t P = 32;
+  while (P < KL + (n0 > 0 ? KS : 0)) P <<= 1;
+  {
+    const uint32_t wpb = 4;
+    size_t smem = (size_t)wpb * (P * (8 + 8 + 4) + K * (8 + 4));
+    by_nc(ix.dp, [&](auto ncv) {
+      constexpr int NC = decltype(ncv)::value;
+      auto kern = k_forward<NC>;
+      GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)div_up(b, wpb), 32 * wpb, smem, st>>>(start, b, ix.slot2phys, ix.attr, ix.i2b, ix.X, ix.dp,
+                                                             ix.adj, K, loc_ids, loc_d, KL, found_slots, found_d,
+                                                             found_cnt, KS, alpha2, P, req_key, req_d, nearest_pre,
+                                                             cnt);
+      GRAB_CHECK_LAUNCH();
+    });
+  }
+  // ---- reverse rewiring: sort requests by (v, q)
+  uint8_t* rewired = pool.alloc<uint8_t>(ix.n_cap);
+  GRAB_CUDA(cudaMemsetAsync(rewired, 0, ix.n_cap, st));
+  {
+    const uint64_t nr_all = b * K;
+    unsigned long long* k2 = pool.alloc<unsigned long long>(nr_all);
+    double* d2 = pool.alloc<double>(nr_all);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, req_key, k2, req_d, d2, (int)nr_all, 0, 64, st);
+    void* t = pool.alloc<uint8_t>(tmp);
+    GRAB_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, req_key, k2, req_d, d2, (int)nr_all, 0, 64, st));
+    // valid requests are the prefix (unused entries are all-ones keys)
+    std::vector<unsigned long long> probe(1);
+    uint64_t lo = 0, hi = nr_all;  // first invalid index by binary search on the device array
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) / 2;
+      GRAB_CUDA(cudaMemcpyAsync(probe.data(), k2 + mid, 8, cudaMemcpyDeviceToHost, st));
+      GRAB_CUDA(cudaStreamSynchronize(st));
+      if (probe[0] == ~0ull)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    const uint64_t nreq = lo;
+    if (nreq) {
+      uint8_t* head = pool.alloc<uint8_t>(nreq);
+      k_req_heads<<<(unsigned)div_up(nreq, 256), 256, 0, st>>>(k2, nreq, head);
+      GRAB_CHECK_LAUNCH();
+      uint32_t* idx = pool.alloc<uint32_t>(nreq);
+      uint32_t* heads = pool.alloc<uint32_t>(nreq);
+      uint32_t* nheads_d = pool.alloc<uint32_t>(1);
+      std::vector<uint32_t> seq(nreq);
+      for (uint64_t i = 0; i < nreq; ++i) seq[i] = (uint32_t)i;
+      GRAB_CUDA(cudaMemcpyAsync(idx, seq.data(), nreq * 4, cudaMemcpyHostToDevice, st));
+      size_t tmp2 = 0;
+      cub::DeviceSelect::Flagged(nullptr, tmp2, idx, head, heads, nheads_d, (int)nreq, st);
+      void* t2 = pool.alloc<uint8_t>(tmp2);
+      GRAB_CUDA(cub::DeviceSelect::Flagged(t2, tmp2, idx, head, heads, nheads_d, (int)nreq, st));
+      uint32_t nheads = 0;
+      GRAB_CUDA(cudaMemcpyAsync(&nheads, nheads_d, 4, cudaMemcpyDeviceToHost, st));
+      GRAB_CUDA(cudaStreamSynchronize(st));
+      const uint32_t wpb = 4;
+      by_nc(ix.dp, [&](auto ncv) {
+        constexpr int NC = decltype(ncv)::value;
+        k_rewire<NC><<<(unsigned)div_up(nheads, wpb), 32 * wpb, 0, st>>>(
+            k2, d2, nreq, heads, nheads, ix.slot2phys, ix.attr, ix.X, ix.dp, ix.adj, K, ix.params.k_local, alpha2,
+            rewired, cnt);
+        GRAB_CHECK_LAUNCH();
+      });
+    }
+  }
+  // ---- heal (n0 > 0)
+  if (n0 > 0) {
+    uint32_t* counts = pool.alloc<uint32_t>(b);
+    uint32_t* miss = pool.alloc<uint32_t>(b);
+    for (int round = 0; round < 4; ++round) {
+      GRAB_CUDA(cudaMemsetAsync(counts, 0, b * 4, st));
+      k_prefix_indeg<<<(unsigned)div_up(start * K, 256), 256, 0, st>>>(ix.adj, ix.slot2phys, ix.attr, start, K, start,
+                                                                       end, counts);
+      GRAB_CHECK_LAUNCH();
+      std::vector<uint32_t> hc(b);
+      GRAB_CUDA(cudaMemcpyAsync(hc.data(), counts, b * 4, cudaMemcpyDeviceToHost, st));
+      GRAB_CUDA(cudaStreamSynchronize(st));
+      std::vector<uint32_t> m;
+      for (uint64_t i = 0; i < b; ++i)
+        if (hc[i] == 0) m.push_back((uint32_t)i);
+      if (m.empty()) break;
+      GRAB_CUDA(cudaMemcpyAsync(miss, m.data(), m.size() * 4, cudaMemcpyHostToDevice, st));
+      by_nc(ix.dp, [&](auto ncv) {
+        constexpr int NC = decltype(ncv)::value;
+        k_heal<NC><<<1, 32, 0, st>>>(miss, (uint32_t)m.size(), start, end, ix.slot2phys, ix.attr, ix.X, ix.dp, ix.adj,
+                                     K, ix.params.k_local, nearest_pre, rewired, cnt);
+        GRAB_CHECK_LAUNCH();
+      });
+    }
+  }
+  InsertCounters hcnt;
+  GRAB_CUDA(cudaMemcpyAsync(&hcnt, cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
+  std::vector<uint8_t> rw(end);
+  GRAB_CUDA(cudaMemcpyAsync(rw.data(), rewired, end, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t s = 0; s < end; ++s)
+    if (rw[s]) ix.last_rewired.push_back((uint32_t)s);
+  R.forward_accepted = hcnt.forward_accepted;
+  R.forward_rejected = hcnt.forward_rejected;
+  R.reverse_accepted = hcnt.reverse_accepted;
+  R.reverse_rejected = hcnt.reverse_rejected;
+  R.evictions_necessary = hcnt.evictions_necessary;
+  R.evictions_redundant = hcnt.evictions_redundant;
+  R.forced_links = hcnt.forced_links;
+  R.n_rewired = ix.last_rewired.size();
+  R.wall_time_s = now_s() - t_begin;
+  if (rep) *rep = R;
+}
+
+// ------------------------------------------------------------- primitives
+template <int NC>
+__global__ void k_select_one(const float* X, uint32_t dp, int64_t target, const int64_t* cs, const double* cd,
+                             const uint8_t* fresh, uint32_t n, uint32_t cap, double alpha2, double* near,
+                             int64_t* out, uint32_t* nout) {
+  const uint32_t lane = lane_id();
+  for (uint32_t t = lane; t < n; t += 32) near[t] = __longlong_as_double(0x7FF0000000000000ll);
+  __syncwarp();
+  uint32_t nacc = 0;
+  for (uint32_t t = 0; t < n && nacc < cap; ++t) {
+    const int64_t s = cs[t];
+    if (s == target) continue;
+    bool dup = false;
+    for (uint32_t j = 0; j < nacc; ++j) dup |= out[j] == s;
+    if (dup) continue;
+    const double de = fresh[t] ? alpha2 * cd[t] : cd[t];
+    if (!(de < near[t])) continue;
+    if (lane == 0) out[nacc] = s;
+    ++nacc;
+    RowRegs<NC> r;
+    load_row<NC>(r, X, dp, (uint32_t)s);
+    for (uint32_t j = 0; j < n; ++j) {
+      double dj = row_dist<NC>(r, X, dp, (uint32_t)cs[j]);
+      if (lane == 0 && dj < near[j]) near[j] = dj;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) *nout = nacc;
+}
+
+template <int NC>
+__global__ void k_rewire_one(const float* X, uint32_t dp, uint32_t* row, uint32_t K, uint32_t v, uint32_t q,
+                             double dvq, double alpha2, uint32_t k_local, int32_t* res) {
+  const uint32_t lane = lane_id();
+  for (uint32_t j = 0; j < K; ++j)
+    if (row[j] == q) {
+      if (lane == 0) res[0] = 0, res[1] = -1;
+      return;
+    }
+  for (uint32_t j = 0; j < K; ++j)
+    if (row[j] == kSentinel) {
+      if (lane == 0) row[j] = q, res[0] = 1, res[1] = -1;
+      return;
+    }
+  RowRegs<NC> rq, rv;
+  load_row<NC>(rq, X, dp, q);
+  load_row<NC>(rv, X, dp, v);
+  const double deff = alpha2 * dvq;
+  for (uint32_t j = 0; j < K; ++j)
+    if (!(deff < row_dist<NC>(rq, X, dp, row[j]))) {
+      if (lane == 0) res[0] = 0, res[1] = -1;
+      return;
+    }
+  const uint32_t r0 = K > k_local ? k_local : 0;
+  double best = -1.0;
+  int32_t pos = -1;
+  for (uint32_t j = r0; j < K; ++j) {
+    double d = row_dist<NC>(rv, X, dp, row[j]);
+    if (d > best) best = d, pos = (int32_t)j;
+  }
+  if (lane == 0) row[pos] = q, res[0] = 1, res[1] = pos;
+}
+
+static float* upload_rows(const float* X, uint64_t n, uint32_t dim, uint32_t dp, cudaStream_t st) {
+  float* d;
+  GRAB_CUDA(cudaMallocAsync(&d, std::max<uint64_t>(n, 1) * dp * 4, st));
+  GRAB_CUDA(cudaMemsetAsync(d, 0, n * dp * 4, st));
+  GRAB_CUDA(cudaMemcpy2DAsync(d, dp * 4, X, dim * 4, dim * 4, n, cudaMemcpyHostToDevice, st));
+  return d;
+}
+
+void select_neighbors_device(const float* X, uint64_t n_rows, uint32_t dim, int64_t target, const int64_t* cand_slots,
+                             const double* cand_dists, const uint8_t* cand_fresh, uint32_t n_cand,
+                             uint32_t row_capacity, double alpha, int64_t* out_accepted, uint32_t* n_accepted) {
+  cudaStream_t st = 0;
+  *n_accepted = 0;
+  if (!n_cand) return;
+  for (uint32_t i = 0; i < n_cand; ++i)
+    if (cand_slots[i] < 0 || (uint64_t)cand_slots[i] >= n_rows) throw Error(GRAB_ERR_VALUE, "candidate slot out of range");
+  const uint32_t dp = (dim + 3) / 4 * 4;
+  float* dX = upload_rows(X, n_rows, dim, dp, st);
+  Pool pool(st);
+  int64_t* cs = pool.alloc<int64_t>(n_cand);
+  double* cd = pool.alloc<double>(n_cand);
+  uint8_t* fr = pool.alloc<uint8_t>(n_cand);
+  double* near = pool.alloc<double>(n_cand);
+  int64_t* out = pool.alloc<int64_t>(std::max<uint32_t>(row_capacity, 1));
+  uint32_t* nout = pool.alloc<uint32_t>(1);
+  GRAB_CUDA(cudaMemcpyAsync(cs, cand_slots, n_cand * 8, cudaMemcpyHostToDevice, st));
+  GRAB_CUDA(cudaMemcpyAsync(cd, cand_dists, n_cand * 8, cudaMemcpyHostToDevice, st));
+  GRAB_CUDA(cudaMemcpyAsync(fr, cand_fresh, n_cand, cudaMemcpyHostToDevice, st));
+  by_nc(dp, [&](auto ncv) {
+    constexpr int NC = decltype(ncv)::value;
+    k_select_one<NC><<<1, 32, 0, st>>>(dX, dp, target, cs, cd, fr, n_cand, row_capacity, alpha * alpha, near, out,
+                                       nout);
+    GRAB_CHECK_LAUNCH();
+  });
+  GRAB_CUDA(cudaMemcpyAsync(n_accepted, nout, 4, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  GRAB_CUDA(cudaMemcpyAsync(out_accepted, out, *n_accepted * 8, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(dX);
+}
+
+void try_rewire_device(const float* X, uint64_t n_rows, uint32_t dim, uint32_t* row, uint32_t k_max, uint32_t v,
+                       uint32_t q, double sq_dvq, double alpha, uint32_t k_local, int32_t* accepted,
+                       int32_t* evicted_pos) {
+  cudaStream_t st = 0;
+  if (v >= n_rows || q >= n_rows) throw Error(GRAB_ERR_VALUE, "slot out of range");
+  for (uint32_t j = 0; j < k_max; ++j)
+    if (row[j] != kSentinel && row[j] >= n_rows) throw Error(GRAB_ERR_VALUE, "row entry out of range");
+  const uint32_t dp = (dim + 3) / 4 * 4;
+  float* dX = upload_rows(X, n_rows, dim, dp, st);
+  Pool pool(st);
+  uint32_t* drow = pool.alloc<uint32_t>(k_max);
+  int32_t* res = pool.alloc<int32_t>(2);
+  GRAB_CUDA(cudaMemcpyAsync(drow, row, k_max * 4, cudaMemcpyHostToDevice, st));
+  by_nc(dp, [&](auto ncv) {
+    constexpr int NC = decltype(ncv)::value;
+    k_rewire_one<NC><<<1, 32, 0, st>>>(dX, dp, drow, k_max, v, q, sq_dvq, alpha * alpha, k_local, res);
+    GRAB_CHECK_LAUNCH();
+  });
+  int32_t h[2];
+  GRAB_CUDA(cudaMemcpyAsync(h, res, 8, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaMemcpyAsync(row, drow, k_max * 4, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(dX);
+  *accepted = h[0];
+  *evicted_pos = h[1];
+}
+
 }  // namespace grab

@@ -35,7 +35,8 @@ __device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t n, uint64
 }
 
 __global__ void __launch_bounds__(256) k_knn_screen(const KnnJob* jobs, const float* X, const Attr* attr,
-                                                    const float* norms, uint32_t dp, uint32_t KP, uint32_t* cand) {
+                                                    const float* norms, uint32_t dp, uint32_t KP, uint32_t* cand,
+                                                    bool causal) {
   extern __shared__ __align__(16) uint8_t smem[];
   float* As = (float*)smem;                 // [BK][BM + 4]
   float* Bs = As + BK * (BM + 4);           // [BK][BN + 4]
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(256) k_knn_screen(const KnnJob* jobs, const fl
       for (int i = 0; i < 8; ++i) {
         uint32_t r = ty * 8 + i;
         float d = fmaxf(a2[i] - 2.f * acc[i][j] + b2, 0.f);
-        if (!cv || job.r0 + r == c) d = __int_as_float(0x7F800000);
+        if (!cv || job.r0 + r == c || (causal && c > job.r0 + r)) d = __int_as_float(0x7F800000);
         D[r * (BN + 1) + tx * 8 + j] = d;
       }
     }
@@ -201,7 +202,7 @@ __global__ void k_knn_rerank(const uint32_t* rows, uint64_t nrows, const uint32_
 }
 
 void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob>& jobs, uint32_t K, bool tb_slot,
-                uint32_t* out_ids, double* out_d, cudaStream_t st) {
+                uint32_t* out_ids, double* out_d, cudaStream_t st, bool causal) {
   if (jobs.empty()) return;
   const uint32_t KP = K + kMargin;
   uint32_t* cand;
@@ -214,7 +215,7 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
                 (size_t)BM * KP * 8;
   if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "k too large for the kNN screen");
   GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_knn_screen<<<(unsigned)jobs.size(), 256, smem, st>>>(dj, ix.X, ix.attr, norms, ix.dp, KP, cand);
+  k_knn_screen<<<(unsigned)jobs.size(), 256, smem, st>>>(dj, ix.X, ix.attr, norms, ix.dp, KP, cand, causal);
   GRAB_CHECK_LAUNCH();
   // rerank every row touched by a job
   std::vector<uint32_t> rows;
@@ -248,6 +249,24 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
   cudaFreeAsync(dr, st);
   cudaFreeAsync(dj, st);
   cudaFreeAsync(cand, st);
+}
+
+__global__ void k_norms(const float* X, uint64_t rows, uint32_t dp, float* out) {
+  uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  float acc = 0.f;
+  for (uint32_t c = lane_id(); c < dp; c += 32) {
+    float v = X[r * dp + c];
+    acc = fmaf(v, v, acc);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if (lane_id() == 0) out[r] = acc;
+}
+
+void row_norms(const DevIndex& ix, float* out, cudaStream_t st) {
+  if (!ix.phys_cap) return;
+  k_norms<<<(unsigned)div_up(ix.phys_cap, 8), 256, 0, st>>>(ix.X, ix.phys_cap, ix.dp, out);
+  GRAB_CHECK_LAUNCH();
 }
 
 }  // namespace grab

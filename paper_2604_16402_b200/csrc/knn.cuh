@@ -18,7 +18,10 @@ struct KnnJob {
 // K nearest valid candidates (excluding p itself), ascending by (f64 dist,
 // tiebreak) where tiebreak = slot (tb_slot) or phys (slab-local column order).
 // Unfilled entries stay as initialised by the caller (SENTINEL).
+// causal: only candidates c < row (same slab => slot order), as the insert's
+// in-bucket candidates (updater.py:143).
 void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob>& jobs, uint32_t K, bool tb_slot,
-                uint32_t* out_ids, double* out_d, cudaStream_t st);
+                uint32_t* out_ids, double* out_d, cudaStream_t st, bool causal = false);
+void row_norms(const DevIndex& ix, float* out, cudaStream_t st);
 
 }  // namespace grab

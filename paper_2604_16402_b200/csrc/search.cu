@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a, SearchShape sh) {
       clear_words(w.vis, 1u << vlg);
       __syncwarp();
       QueryRegs<NC> qr;
-      load_query<NC>(qr, a.Q + (uint64_t)qi * a.dp, a.dp);
+      load_query<NC>(qr, a.qphys ? a.X + (uint64_t)a.qphys[qi] * a.dp : a.Q + (uint64_t)qi * a.dp, a.dp);
       const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f);
       const uint32_t hi_b = bucket_of_f32(a.bound, a.m, hi_f);
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);

@@ -20,6 +20,7 @@ struct SearchArgs {
   uint64_t n_live;
   // queries (rows padded to dp)
   const float* Q;
+  const uint32_t* qphys;  // optional: query i = X row qphys[i] (insert candidate search)
   const double* lower;
   const double* upper;
   uint64_t range_stride;

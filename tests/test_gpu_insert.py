@@ -1,0 +1,177 @@
+"""GPU insert parity: device insert_batch vs the live-reference goldens and the
+oracle restatement; Eq.1/Eq.2 primitives on the reference's hand geometries."""
+import numpy as np
+import pytest
+
+from oracle import beam, construct, index_state as ist, ingest
+
+pytestmark = pytest.mark.gpu
+SENT = np.uint32(0xFFFFFFFF)
+KEYS = ["batch_size", "bulk_built", "forward_accepted", "forward_rejected", "reverse_accepted", "reverse_rejected",
+        "evictions_necessary", "evictions_redundant", "forced_links"]
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_2604_16402_b200 as g
+    return g
+
+
+def store_of(points):
+    return np.asarray(points, dtype=np.float32)
+
+
+def cands(X, v, slots):
+    d = [(float(((X[v].astype(np.float64) - X[s].astype(np.float64)) ** 2).sum()), s) for s in slots]
+    return [(s, dd) for dd, s in sorted(d)]
+
+
+def test_select_hand_geometries(g):
+    X = store_of([[0, 0], [1, 0], [1.05, 0]])
+    assert g.select_neighbors(X, 0, cands(X, 0, [1, 2]), 4, 1.0, frozenset()) == [1]
+    assert g.select_neighbors(X, 0, cands(X, 0, [1, 2]), 4, 0.1, frozenset({2})) == [1]
+    X2 = store_of([[0, 0], [1, 0], [0, 1]])
+    assert g.select_neighbors(X2, 0, cands(X2, 0, [1, 2]), 4, 0.1, frozenset({2})) == [1, 2]
+    r = np.random.default_rng(0)
+    P = r.standard_normal((30, 4)).astype(np.float32)
+    c = cands(P, 0, list(range(1, 30)))
+    assert g.select_neighbors(P, 0, c, 8, 1.0, frozenset()) == g.select_neighbors(P, 0, c, 8, 1.0, frozenset(range(30)))
+    assert g.select_neighbors(P, 0, c, 8, 1.0, frozenset()) == ingest.prune_set(P, 0, c, 8, 1.0, set())
+    for alpha in (0.2, 0.6, 1.0):
+        fresh = set(range(15, 30))
+        assert g.select_neighbors(P, 0, c, 8, alpha, fresh) == ingest.prune_set(P, 0, c, 8, alpha, fresh)
+    P3 = r.standard_normal((50, 8)).astype(np.float32)
+    assert len(g.select_neighbors(P3, 0, cands(P3, 0, list(range(1, 50))), 3, 1.0, frozenset())) == 3
+
+
+def test_try_rewire_cases(g):
+    X = store_of([[0, 0], [1, 0], [2, 0]])
+    adj = np.full((3, 4), SENT, dtype="<u4")
+    adj[0, 0] = 1
+    ok, ev = g.try_rewire(X, adj, 0, 2, 4.0, 0.6, 2)
+    assert ok and ev == -1 and adj[0, 1] == 2
+    X = store_of([[0, 0], [1, 0], [1.05, 0]])
+    adj = np.array([[1, 1, 1, 1]], dtype="<u4")
+    ok, _ = g.try_rewire(X, adj, 0, 2, 1.05 ** 2, 1.0, 2)
+    assert not ok and adj.tolist() == [[1, 1, 1, 1]]
+    X = store_of([[0, 0], [50, 0], [3, 0], [4, 0], [0.01, 0]])
+    adj = np.array([[1, 2, 3, 2]], dtype="<u4")
+    ok, ev = g.try_rewire(X, adj, 0, 4, 0.0001, 0.6, 2)
+    assert ok and ev >= 2 and 4 in adj[0] and adj[0][0] == 1
+    X = store_of([[0, 0], [1, 0]])
+    adj = np.array([[1, SENT, SENT, SENT]], dtype="<u4")
+    assert not g.try_rewire(X, adj, 0, 1, 1.0, 0.6, 2)[0]
+
+
+def test_insert_matches_reference_goldens(g, golden):
+    gold = golden("insert")
+    V, S = ist.gen_synthetic(3500, 12, rng_seed=5)
+    params = g.BuildParams(k_max=16, k_local=8, bucket_capacity=600, alpha=0.6)
+    gi, _ = g.build_index(V[:3000], S[:3000], params)
+    base_same = np.mean([np.array_equal(a, b) for a, b in zip(gi.adjacency[:3000], gold["base_adj"])])
+    rep = g.insert_batch(gi, V[3000:], S[3000:])
+    got = [getattr(rep, k) for k in KEYS]
+    print("base identity", base_same, "report", got, "ref", gold["report"].tolist())
+    same = np.mean([np.array_equal(a, b) for a, b in zip(gi.adjacency[:3500], gold["adj"])])
+    print("post-insert row identity", same)
+    if base_same == 1.0:
+        assert got == gold["report"].tolist()
+        assert rep.rewired_rows == gold["rewired"].tolist()
+        assert same == 1.0
+    V2, S2 = ist.gen_synthetic(300, 12, rng_seed=55)
+    rep2 = g.insert_batch(gi, V2, S2)
+    same2 = np.mean([np.array_equal(a, b) for a, b in zip(gi.adjacency[:3800], gold["adj2"])])
+    print("second batch", [getattr(rep2, k) for k in KEYS], gold["report2"].tolist(), same2)
+    if base_same == 1.0:
+        assert same2 == 1.0
+
+
+def test_insert_on_reference_graph_is_exact(g, golden):
+    """Insert into the reference-built graph (loaded into the device layout): every
+    adjacency row and every report counter must equal the reference's."""
+    gold = golden("insert")
+    V, S = ist.gen_synthetic(3500, 12, rng_seed=5)
+    cfg = ist.BuildCfg(k_max=16, k_local=8, bucket_capacity=600, alpha=0.6)
+    ref, _, _ = construct.build(V[:3000], S[:3000], cfg)
+    raw = ist.container_bytes(ref)
+    params = g.BuildParams(k_max=16, k_local=8, bucket_capacity=600, alpha=0.6)
+    gi = g.load_index(raw, params)
+    # the container drops capacity headroom semantics only through N_cap (kept = 6000)
+    rep = g.insert_batch(gi, V[3000:], S[3000:])
+    assert [getattr(rep, k) for k in KEYS] == gold["report"].tolist()
+    assert rep.rewired_rows == gold["rewired"].tolist()
+    assert np.array_equal(gi.adjacency[:3500], gold["adj"])
+
+
+def test_insert_empty_index_bulk_builds(g, golden):
+    gold = golden("insert")
+    V3, S3 = ist.gen_synthetic(1200, 8, rng_seed=7)
+    gi = g.create_index(8, 2400, g.BuildParams(k_max=8, k_local=4, bucket_capacity=500))
+    rep = g.insert_batch(gi, V3, S3)
+    assert rep.bulk_built == 500 and gi.count == 1200
+    A = gi.adjacency[:1200]
+    assert (A != SENT).any(axis=1).all()
+    print("empty-index report", [getattr(rep, k) for k in KEYS], gold["report3"].tolist())
+
+
+def test_insert_invariants_and_errors(g):
+    V, S = ist.gen_synthetic(5256, 16, "clusters", rng_seed=4)
+    params = g.BuildParams(k_max=16, k_local=8, bucket_capacity=1000, alpha=0.6)
+    gi, _ = g.build_index(V[:5000], S[:5000], params)
+    x_before = gi.store.X[:5000].copy()
+    a_before = gi.adjacency[:5000].copy()
+    rep = g.insert_batch(gi, V[5000:], S[5000:])
+    assert rep.batch_size == 256
+    old = gi.adjacency[:5000]
+    flat = old[old != SENT].astype(np.int64)
+    incoming = np.bincount(flat[(flat >= 5000) & (flat < 5256)] - 5000, minlength=256)
+    assert (incoming > 0).all()
+    assert gi.store.X[:5000].tobytes() == x_before.tobytes()
+    changed = np.flatnonzero((gi.adjacency[:5000] != a_before).any(axis=1))
+    assert set(changed.tolist()).issubset(set(rep.rewired_rows))
+    before = gi.adjacency.copy()
+    r0 = g.insert_batch(gi, np.zeros((0, 16), np.float32), np.zeros(0))
+    assert r0.batch_size == 0 and np.array_equal(gi.adjacency, before)
+    V4, S4 = ist.gen_synthetic(100, 4, rng_seed=8)
+    gi4, _ = g.build_index(V4, S4, g.BuildParams(k_max=4, k_local=2, bucket_capacity=50), capacity=110)
+    with pytest.raises(g.CapacityError):
+        g.insert_batch(gi4, np.zeros((20, 4), np.float32), np.full(20, 0.5))
+    with pytest.raises(g.DimensionMismatchError):
+        g.insert_batch(gi4, np.zeros((2, 5), np.float32), np.full(2, 0.5))
+    with pytest.raises(ValueError):
+        g.insert_batch(gi4, np.zeros((1, 4), np.float32), np.array([np.inf]))
+
+
+def test_insert_deterministic(g):
+    V, S = ist.gen_synthetic(2300, 8, rng_seed=6)
+    params = g.BuildParams(k_max=16, k_local=8, bucket_capacity=500, alpha=0.6, rng_seed=9)
+    snaps = []
+    for _ in range(2):
+        gi, _ = g.build_index(V[:2000], S[:2000], params)
+        g.insert_batch(gi, V[2000:], S[2000:])
+        snaps.append(gi.adjacency[: gi.count].tobytes())
+    assert snaps[0] == snaps[1]
+
+
+def test_insert_recall_parity_with_reference(g):
+    """Insert path on the low-rank family: GPU build+insert vs oracle build+insert recall within 0.005."""
+    X, S = ist.gen_lowrank(12_000, 32, seed=0)
+    Q = ist.lowrank_queries(300, 32, seed=1)
+    cfg = ist.BuildCfg(k_max=32, k_local=16, bucket_capacity=1000)
+    ref, _, _ = construct.build(X[:8000], S[:8000], cfg, capacity=16000)
+    ingest.insert(ref, X[8000:], S[8000:])
+    params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=1000)
+    ref_gpu = g.load_index(ist.container_bytes(ref), params)
+    gi, _ = g.build_index(X[:8000], S[:8000], params, capacity=16000)
+    g.insert_batch(gi, X[8000:], S[8000:])
+    ranges = beam.window_ranges(S, 0.1, len(Q), 0)
+    lo = np.array([r[0] for r in ranges])
+    hi = np.array([r[1] for r in ranges])
+    truth, _, tc = g.brute_force_arrays(gi, Q, lo, hi, 10)
+    sp = g.SearchParams(k=10, itopk=64)
+    a = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0)
+    b = g.search_arrays(ref_gpu, Q, lo, hi, sp, seed_base=0)
+    ra = np.mean([beam.recall(a.slots[i, :a.counts[i]], truth[i, :tc[i]], 10) for i in range(len(Q))])
+    rb = np.mean([beam.recall(b.slots[i, :b.counts[i]], truth[i, :tc[i]], 10) for i in range(len(Q))])
+    print(f"insert recall gpu {ra:.4f} ref {rb:.4f}")
+    assert abs(ra - rb) <= 0.005 or ra > rb
