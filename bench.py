@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--target", type=float, default=0.95)
     ap.add_argument("--cpu-sample", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--insert-batch", type=int, default=100_000)
     args = ap.parse_args()
     cfg = dict(PRESETS[args.config])
     for key in ("n", "dim", "cap", "nq", "sel"):
@@ -307,12 +308,29 @@ def main():
     h2d = Q.nbytes + lo.nbytes + hi.nbytes
     d2h = rh.slots.nbytes + rh.dists.nbytes + rh.counts.nbytes
 
+    # the CPU baseline searches the same graph: export it before the insert mutates it
+    cpu_idx = oracle_index_from(gi) if (rank == 0 and world == 1 and not args.no_cpu) else None
+
+    # ---- insert vectors/s: one append-only batch into the built index (N_cap = 2n)
+    ins_b = min(args.insert_batch, gi.capacity - gi.count)
+    Xi, Si = ds.gen_lowrank(ins_b, dim, seed=2)
+    Xi_d = torch.from_numpy(Xi).to(dev)
+    Si_d = torch.from_numpy(Si).to(dev)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    irep = g.insert_batch(gi, Xi_d, Si_d)
+    torch.cuda.synchronize()
+    ins_s = time.perf_counter() - t2
+    insert_vps = ins_b / ins_s
+
     line = {"metric": "range-filtered QPS @ recall@10=0.95", "value": round(qps, 1), "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 accumulate / f32 storage",
             "data": "synthetic (low-rank-16, seeds 0/1; see config)", "config": config,
             "build_s": round(build_s, 3), "build_report": brep.to_dict() | {"bucket_sizes": None},
-            "insert_vectors_per_s": None,
+            "insert_vectors_per_s": round(insert_vps, 1),
+            "insert": {"batch": ins_b, "seconds": round(ins_s, 4), "into": n,
+                       "report": {k: v for k, v in irep.to_dict().items() if k != "rewired_rows"}},
             "e2e": {"value": round(world * nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -320,17 +338,29 @@ def main():
                          "kernel": "k_search (filtered beam search)",
                          "bytes_per_query": round(bytes_q / nq, 1)},
             "gpu_launches": args.steps, "clocks": clk.summary(), "sweep": sweep}
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if cpu_idx is not None:
         procs = os.cpu_count() or 1
-        idx = oracle_index_from(gi)
+        idx = cpu_idx
         m = min(args.cpu_sample, nq)
         seeds = [int(np.random.SeedSequence([seed_base, i]).generate_state(1, np.uint64)[0]) for i in range(m)]
         cq, cel, cslots = cpu_search_qps(idx, Q[:m], lo[:m], hi[:m], seeds, (itopk, width, iters), procs, 1)
         agree = np.mean([cslots[i] == res.slots[i, : int(res.counts[i])].tolist() for i in range(m)])
+        from oracle import ingest
+        ci = min(200, ins_b)
+        idx.X = np.concatenate([idx.X, np.zeros((ci, dim), np.float32)])
+        idx.scalars = np.concatenate([idx.scalars, np.zeros(ci, np.float32)])
+        idx.ids = np.arange(len(idx.X))
+        idx.adjacency = np.concatenate([idx.adjacency, np.full((ci, 32), 0xFFFFFFFF, np.uint32)])
+        idx.i2b = np.concatenate([idx.i2b, np.full(ci, -1, np.int32)])
+        tci = time.perf_counter()
+        ingest.insert(idx, Xi[:ci], Si[:ci])
+        cpu_ins = ci / (time.perf_counter() - tci)
         line["cpu_baseline"] = {"value": round(cq, 2), "unit": "queries/s", "cores": procs, "kind": "port",
                                 "sample": f"{m} of the {nq} queries, numpy port of searcher.py (oracle/beam.py), "
                                           f"fork pool of {procs}, same graph and params",
-                                "result_agreement": float(agree)}
+                                "result_agreement": float(agree),
+                                "insert_vectors_per_s": round(cpu_ins, 2),
+                                "insert_sample": f"{ci} vectors into the same {n}-row graph, single process"}
     if rank == 0:
         print(json.dumps(line))
     if dist:

@@ -84,6 +84,9 @@ typedef struct {
   uint64_t reverse_accepted, reverse_rejected, evictions_necessary, evictions_redundant;
   uint64_t forced_links, n_rewired;
   double wall_time_s;
+  /* seconds: append, in-bucket candidates, candidate search, forward selection,
+   * reverse rewiring, healing */
+  double phase_seconds[6];
 } grab_insert_report;
 
 typedef struct {

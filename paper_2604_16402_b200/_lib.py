@@ -58,7 +58,8 @@ class BuildDebugC(C.Structure):
 
 
 class InsertReportC(C.Structure):
-    _fields_ = [(f, C.c_uint64) for f in INSERT_FIELDS] + [("wall_time_s", C.c_double)]
+    _fields_ = [(f, C.c_uint64) for f in INSERT_FIELDS] + [("wall_time_s", C.c_double),
+                                                          ("phase_seconds", C.c_double * 6)]
 
 
 class InfoC(C.Structure):

@@ -353,9 +353,13 @@ class InsertReport:
     forced_links: int = 0
     rewired_rows: list = field(default_factory=list)
     wall_time_s: float = 0.0
+    phase_seconds: dict = field(default_factory=dict)
 
     def to_dict(self) -> dict:
         return dict(self.__dict__)
+
+
+_INSERT_PHASES = ["append", "bucket_candidates", "candidate_search", "forward_select", "reverse_rewire", "heal"]
 
 
 def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk: int = 128) -> InsertReport:
@@ -402,7 +406,8 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
                         reverse_accepted=int(rep.reverse_accepted), reverse_rejected=int(rep.reverse_rejected),
                         evictions_necessary=int(rep.evictions_necessary),
                         evictions_redundant=int(rep.evictions_redundant), forced_links=int(rep.forced_links),
-                        rewired_rows=[int(x) for x in rw], wall_time_s=float(rep.wall_time_s))
+                        rewired_rows=[int(x) for x in rw], wall_time_s=float(rep.wall_time_s),
+                        phase_seconds={k: float(rep.phase_seconds[i]) for i, k in enumerate(_INSERT_PHASES)})
 
 
 def _rows_of(store) -> np.ndarray:

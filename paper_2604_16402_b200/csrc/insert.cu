@@ -328,54 +328,72 @@ __global__ void k_prefix_indeg(const uint32_t* adj, const uint32_t* s2p, const A
   if (s >= start && s < end) atomicAdd(counts + (s - start), 1u);
 }
 
+// _heal_unreachable decisions: the target row v of a missing newcomer q depends
+// only on q's own (fresh, unchanging) row and nearest_pre, so all choices are
+// made in parallel; rows v are then patched serially per v, in q order.
 template <int NC>
-__global__ void k_heal(const uint32_t* missing, uint32_t nmiss, uint64_t start, uint64_t end, const uint32_t* s2p,
-                       const Attr* attr, const float* X, uint32_t dp, uint32_t* adj, uint32_t K, uint32_t k_local,
-                       const uint32_t* nearest_pre, uint8_t* rewired_slot, InsertCounters* cnt) {
-  const uint32_t lane = lane_id();
-  for (uint32_t t = 0; t < nmiss; ++t) {
-    const uint64_t q = start + missing[t];
-    const uint32_t pq = s2p[q];
-    const uint32_t* rq = adj + (uint64_t)pq * K;
-    RowRegs<NC> qr;
-    load_row<NC>(qr, X, dp, pq);
-    // nearest pre-batch entry of q's own row, ties by slot
-    double bd = __longlong_as_double(0x7FF0000000000000ll);
-    uint32_t v = kSentinel;
-    for (uint32_t j = 0; j < K; ++j) {
-      uint32_t e = rq[j];
-      if (e == kSentinel) continue;
-      uint32_t s = attr[e].slot;
-      if (s >= start) continue;
-      double d = row_dist<NC>(qr, X, dp, e);
-      if (key_less(d, s, bd, v)) {
-        bd = d;
-        v = s;
-      }
+__global__ void k_heal_choose(const uint32_t* missing, uint32_t nmiss, uint64_t start, const uint32_t* s2p,
+                              const Attr* attr, const float* X, uint32_t dp, const uint32_t* adj, uint32_t K,
+                              const uint32_t* nearest_pre, unsigned long long* keys) {
+  const uint32_t wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const uint64_t t = blockIdx.x * (uint64_t)wpb + wib;
+  if (t >= nmiss) return;
+  const uint64_t q = start + missing[t];
+  const uint32_t pq = s2p[q];
+  const uint32_t* rq = adj + (uint64_t)pq * K;
+  RowRegs<NC> qr;
+  load_row<NC>(qr, X, dp, pq);
+  double bd = __longlong_as_double(0x7FF0000000000000ll);
+  uint32_t v = kSentinel;
+  for (uint32_t j = 0; j < K; ++j) {
+    const uint32_t e = rq[j];
+    if (e == kSentinel) continue;
+    const uint32_t s = attr[e].slot;
+    if (s >= start) continue;
+    const double d = row_dist<NC>(qr, X, dp, e);
+    if (key_less(d, s, bd, v)) {
+      bd = d;
+      v = s;
     }
-    if (v == kSentinel) v = nearest_pre[missing[t]];
-    if (v == kSentinel) continue;
-    const uint32_t pv = s2p[v];
-    uint32_t* row = adj + (uint64_t)pv * K;
+  }
+  if (v == kSentinel) v = nearest_pre[missing[t]];
+  if (lane_id() == 0) keys[t] = v == kSentinel ? ~0ull : (((unsigned long long)v << 32) | (unsigned long long)q);
+}
+
+template <int NC>
+__global__ void k_heal_apply(const unsigned long long* keys, uint64_t nreq, const uint32_t* heads, uint32_t nheads,
+                             uint64_t start, uint64_t end, const uint32_t* s2p, const Attr* attr, const float* X,
+                             uint32_t dp, uint32_t* adj, uint32_t K, uint32_t k_local, uint8_t* rewired_slot,
+                             InsertCounters* cnt) {
+  const uint32_t wib = threadIdx.x >> 5, lane = lane_id(), wpb = blockDim.x >> 5;
+  const uint64_t h = blockIdx.x * (uint64_t)wpb + wib;
+  if (h >= nheads) return;
+  const uint64_t b0 = heads[h], b1 = h + 1 < nheads ? heads[h + 1] : nreq;
+  const uint32_t v = (uint32_t)(keys[b0] >> 32);
+  const uint32_t pv = s2p[v];
+  uint32_t* row = adj + (uint64_t)pv * K;
+  RowRegs<NC> vr;
+  load_row<NC>(vr, X, dp, pv);
+  unsigned long long forced = 0, evict = 0;
+  for (uint64_t r = b0; r < b1; ++r) {
+    const uint32_t pq = s2p[(uint32_t)keys[r]];
     int32_t free_pos = -1;
-    for (uint32_t j = 0; j < K; ++j)
-      if (row[j] == kSentinel) {
-        free_pos = (int32_t)j;
-        break;
-      }
+    for (uint32_t c0 = 0; c0 < K && free_pos < 0; c0 += 32) {
+      uint32_t c = c0 + lane;
+      uint32_t fm = __ballot_sync(0xFFFFFFFFu, c < K && row[c] == kSentinel);
+      if (fm) free_pos = (int32_t)(c0 + __ffs(fm) - 1);
+    }
     if (free_pos >= 0) {
       __syncwarp();
       if (lane == 0) row[free_pos] = pq;
     } else {
       const uint32_t r0 = K > k_local ? k_local : 0;
-      RowRegs<NC> vr;
-      load_row<NC>(vr, X, dp, pv);
       double best_st = -1.0, best_any = -1.0;
       int32_t pos_st = -1, pos_any = -1;
       for (uint32_t j = r0; j < K; ++j) {
-        uint32_t e = row[j];
-        double d = row_dist<NC>(vr, X, dp, e);
-        uint32_t s = attr[e].slot;
+        const uint32_t e = row[j];
+        const double d = row_dist<NC>(vr, X, dp, e);
+        const uint32_t s = attr[e].slot;
         if (d > best_any) {
           best_any = d;
           pos_any = (int32_t)j;
@@ -387,15 +405,62 @@ __global__ void k_heal(const uint32_t* missing, uint32_t nmiss, uint64_t start, 
       }
       __syncwarp();
       if (lane == 0) row[pos_st >= 0 ? pos_st : pos_any] = pq;
-      if (lane == 0) cnt->evictions_redundant += 1;
+      ++evict;
     }
     __syncwarp();
-    if (lane == 0) {
-      cnt->forced_links += 1;
-      rewired_slot[v] = 1;
-    }
-    __syncwarp();
+    ++forced;
   }
+  if (lane == 0) {
+    atomicAdd(&cnt->forced_links, forced);
+    atomicAdd(&cnt->evictions_redundant, evict);
+    rewired_slot[v] = 1;
+  }
+}
+
+// Sorted u64 keys (valid prefix, ~0 padding) -> number of valid keys and the
+// start index of every run with equal high 32 bits.
+static uint64_t segment_heads(Pool& pool, const unsigned long long* keys, uint64_t n, uint32_t** heads_out,
+                              uint32_t* nheads_out, cudaStream_t st) {
+  uint64_t lo = 0, hi = n;
+  unsigned long long probe = 0;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) / 2;
+    GRAB_CUDA(cudaMemcpyAsync(&probe, keys + mid, 8, cudaMemcpyDeviceToHost, st));
+    GRAB_CUDA(cudaStreamSynchronize(st));
+    if (probe == ~0ull)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const uint64_t nv = lo;
+  *nheads_out = 0;
+  if (!nv) return 0;
+  uint8_t* head = pool.alloc<uint8_t>(nv);
+  k_req_heads<<<(unsigned)div_up(nv, 256), 256, 0, st>>>(keys, nv, head);
+  GRAB_CHECK_LAUNCH();
+  uint32_t* idx = pool.alloc<uint32_t>(nv);
+  std::vector<uint32_t> seq(nv);
+  for (uint64_t i = 0; i < nv; ++i) seq[i] = (uint32_t)i;
+  GRAB_CUDA(cudaMemcpyAsync(idx, seq.data(), nv * 4, cudaMemcpyHostToDevice, st));
+  uint32_t* heads = pool.alloc<uint32_t>(nv);
+  uint32_t* nh = pool.alloc<uint32_t>(1);
+  size_t tmp = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp, idx, head, heads, nh, (int)nv, st);
+  void* t = pool.alloc<uint8_t>(tmp);
+  GRAB_CUDA(cub::DeviceSelect::Flagged(t, tmp, idx, head, heads, nh, (int)nv, st));
+  GRAB_CUDA(cudaMemcpyAsync(nheads_out, nh, 4, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  *heads_out = heads;
+  return nv;
+}
+
+static unsigned long long* sort_keys(Pool& pool, unsigned long long* keys, uint64_t n, cudaStream_t st) {
+  unsigned long long* out = pool.alloc<unsigned long long>(n);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, out, (int)n, 0, 64, st);
+  void* t = pool.alloc<uint8_t>(tmp);
+  GRAB_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, keys, out, (int)n, 0, 64, st));
+  return out;
 }
 
 // ------------------------------------------------------------- driver
@@ -473,12 +538,20 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
                                        " requested > " + std::to_string(ix.n_cap));
   const uint64_t start = n0, end = n0 + b;
   const uint32_t K = ix.params.k_max;
+  double tp = now_s();
+  auto mark = [&](int ph) {
+    GRAB_CUDA(cudaStreamSynchronize(st));
+    double t = now_s();
+    R.phase_seconds[ph] += t - tp;
+    tp = t;
+  };
   // ---- append (bucket ids, zero-shift placement)
   launch_bucket_ids(ix, Sd, b, ix.i2b + start, st);
   std::vector<uint32_t> old_count = ix.h_bcount;
   layout_append(ix, Vd, Sd, start, b);
   for (uint64_t i = 0; i < b; ++i) ix.ids[start + i] = ids ? ids[i] : (int64_t)(start + i);
 
+  mark(0);
   // ---- in-bucket candidates: causal kNN over each touched slab
   const uint32_t KL = 2 * K;
   uint32_t* loc_ids = pool.alloc<uint32_t>(ix.phys_cap * (uint64_t)KL);
@@ -495,6 +568,7 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
     }
     knn_device(ix, norms, jobs, KL, /*tb_slot=*/false, loc_ids, loc_d, st, /*causal=*/true);
   }
+  mark(1);
   // ---- full-range graph search over the pre-batch prefix
   const uint32_t KS = search_itopk;
   int64_t* found_slots = nullptr;
@@ -544,6 +618,7 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
     a.out_stats = nullptr;
     run_search(ix, a, st);
   }
+  mark(2);
   // ---- forward selection
   const double alpha2 = ix.params.alpha * ix.params.alpha;
   InsertCounters* cnt = pool.alloc<InsertCounters>(1);
@@ -568,6 +643,7 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
       GRAB_CHECK_LAUNCH();
     });
   }
+  mark(3);
   // ---- reverse rewiring: sort requests by (v, q)
   uint8_t* rewired = pool.alloc<uint8_t>(ix.n_cap);
   GRAB_CUDA(cudaMemsetAsync(rewired, 0, ix.n_cap, st));
@@ -619,10 +695,12 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
       });
     }
   }
+  mark(4);
   // ---- heal (n0 > 0)
   if (n0 > 0) {
     uint32_t* counts = pool.alloc<uint32_t>(b);
     uint32_t* miss = pool.alloc<uint32_t>(b);
+    unsigned long long* hkeys = pool.alloc<unsigned long long>(b);
     for (int round = 0; round < 4; ++round) {
       GRAB_CUDA(cudaMemsetAsync(counts, 0, b * 4, st));
       k_prefix_indeg<<<(unsigned)div_up(start * K, 256), 256, 0, st>>>(ix.adj, ix.slot2phys, ix.attr, start, K, start,
@@ -635,15 +713,29 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
       for (uint64_t i = 0; i < b; ++i)
         if (hc[i] == 0) m.push_back((uint32_t)i);
       if (m.empty()) break;
-      GRAB_CUDA(cudaMemcpyAsync(miss, m.data(), m.size() * 4, cudaMemcpyHostToDevice, st));
+      const uint32_t nm = (uint32_t)m.size();
+      GRAB_CUDA(cudaMemcpyAsync(miss, m.data(), nm * 4, cudaMemcpyHostToDevice, st));
       by_nc(ix.dp, [&](auto ncv) {
         constexpr int NC = decltype(ncv)::value;
-        k_heal<NC><<<1, 32, 0, st>>>(miss, (uint32_t)m.size(), start, end, ix.slot2phys, ix.attr, ix.X, ix.dp, ix.adj,
-                                     K, ix.params.k_local, nearest_pre, rewired, cnt);
+        k_heal_choose<NC><<<(unsigned)div_up(nm, 4), 128, 0, st>>>(miss, nm, start, ix.slot2phys, ix.attr, ix.X,
+                                                                    ix.dp, ix.adj, K, nearest_pre, hkeys);
+        GRAB_CHECK_LAUNCH();
+      });
+      unsigned long long* sk = sort_keys(pool, hkeys, nm, st);
+      uint32_t* heads = nullptr;
+      uint32_t nheads = 0;
+      const uint64_t nv = segment_heads(pool, sk, nm, &heads, &nheads, st);
+      if (!nv) continue;
+      by_nc(ix.dp, [&](auto ncv) {
+        constexpr int NC = decltype(ncv)::value;
+        k_heal_apply<NC><<<(unsigned)div_up(nheads, 4), 128, 0, st>>>(sk, nv, heads, nheads, start, end, ix.slot2phys,
+                                                                      ix.attr, ix.X, ix.dp, ix.adj, K,
+                                                                      ix.params.k_local, rewired, cnt);
         GRAB_CHECK_LAUNCH();
       });
     }
   }
+  mark(5);
   InsertCounters hcnt;
   GRAB_CUDA(cudaMemcpyAsync(&hcnt, cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
   std::vector<uint8_t> rw(end);

@@ -175,3 +175,17 @@ def test_insert_recall_parity_with_reference(g):
     rb = np.mean([beam.recall(b.slots[i, :b.counts[i]], truth[i, :tc[i]], 10) for i in range(len(Q))])
     print(f"insert recall gpu {ra:.4f} ref {rb:.4f}")
     assert abs(ra - rb) <= 0.005 or ra > rb
+
+
+def test_insert_scaled_matches_oracle(g):
+    """10 % batch into a 10K reference graph: counters (incl. forced links) and rows equal the oracle's."""
+    X, S = ist.gen_lowrank(11_000, 24, seed=3)
+    cfg = ist.BuildCfg(k_max=32, k_local=16, bucket_capacity=1000)
+    ref, _, _ = construct.build(X[:10_000], S[:10_000], cfg, capacity=12_000)
+    gi = g.load_index(ist.container_bytes(ref), g.BuildParams(k_max=32, k_local=16, bucket_capacity=1000))
+    rep = g.insert_batch(gi, X[10_000:], S[10_000:])
+    t = ingest.insert(ref, X[10_000:], S[10_000:])
+    print("gpu", [getattr(rep, k) for k in KEYS], "oracle", [getattr(t, k) for k in KEYS], rep.phase_seconds)
+    assert [getattr(rep, k) for k in KEYS] == [getattr(t, k) for k in KEYS]
+    assert rep.rewired_rows == t.rewired_rows
+    assert np.array_equal(gi.adjacency[:11_000], ref.adjacency[:11_000])

@@ -1,0 +1,18 @@
+"""Build cfg2-shape index and insert one batch; print the insert phase timings."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_16402_b200 as g  # noqa: E402
+from paper_2604_16402_b200 import datasets as ds  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+b = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
+X, S = ds.gen_lowrank(n, 128, seed=0)
+gi, rep = g.build_index(X, S, g.BuildParams(k_max=32, k_local=16, bucket_capacity=10_000))
+print("build", rep.to_dict() | {"bucket_sizes": None})
+Xi, Si = ds.gen_lowrank(b, 128, seed=2)
+r = g.insert_batch(gi, Xi, Si)
+d = r.to_dict()
+d.pop("rewired_rows")
+print("insert", d)
