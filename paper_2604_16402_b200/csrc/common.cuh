@@ -76,9 +76,85 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Reduce G per-lane partials (G candidates) at once with the SAME pairing tree
+// as warp_sum (i^16, ^8, ^4, ^2, ^1): the first log2(G) levels scatter halves
+// of the candidate set between partner lanes, the rest all-reduce. Lane i ends
+// with the full sum of candidate (i >> (5 - log2 G)); bit-identical to
+// warp_sum(p[g]) because every level adds the same operand pair.
+// Shuffles: 18 (G=8), 20 (G=4), 18 (G=2) double-words vs 10*G for warp_sum.
+template <int G>
+__device__ __forceinline__ double reduce_scatter(double (&p)[G]) {
+  const uint32_t lane = threadIdx.x & 31u;
+  if constexpr (G == 1) {
+    return warp_sum(p[0]);
+  } else {
+    constexpr int H = G / 2;
+    constexpr uint32_t OFF = 16;
+    const bool hi = (lane & OFF) != 0;
+    double q[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const double send = hi ? p[j] : p[H + j];
+      const double keep = hi ? p[H + j] : p[j];
+      q[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, OFF);
+    }
+    if constexpr (H == 1) {
+      double t = q[0];
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+      return t;
+    } else {
+      constexpr int H2 = H / 2;
+      const bool hi2 = (lane & 8u) != 0;
+      double r[H2];
+#pragma unroll
+      for (int j = 0; j < H2; ++j) {
+        const double send = hi2 ? q[j] : q[H2 + j];
+        const double keep = hi2 ? q[H2 + j] : q[j];
+        r[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 8);
+      }
+      if constexpr (H2 == 1) {
+        double t = r[0];
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+        return t;
+      } else {
+        static_assert(H2 == 2, "G <= 8");
+        const bool hi3 = (lane & 4u) != 0;
+        const double send = hi3 ? r[0] : r[1];
+        const double keep = hi3 ? r[1] : r[0];
+        double t = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 4);
+        t += __shfl_xor_sync(0xFFFFFFFFu, t, 2);
+        t += __shfl_xor_sync(0xFFFFFFFFu, t, 1);
+        return t;
+      }
+    }
+  }
+}
+
 // Total order used for every (distance, slot) decision (SPEC tie rule).
 __device__ __forceinline__ bool key_less(double da, uint32_t sa, double db, uint32_t sb) {
   return da < db || (da == db && sa < sb);
 }
 
+}  // namespace grab
+
+namespace grab {
+// Growable stream-ordered device scratch buffer.
+struct DBufLite {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaStream_t st = nullptr;
+  void ensure(size_t bytes, cudaStream_t s) {
+    if (bytes <= cap && p) return;
+    if (p) cudaFreeAsync(p, st);
+    st = s;
+    p = nullptr;
+    GRAB_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, s));
+    cap = bytes;
+  }
+  ~DBufLite() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
 }  // namespace grab

@@ -89,6 +89,13 @@ extern "C" int grab_create(int device, uint32_t dim, uint64_t capacity, const gr
     GRAB_CUDA(cudaSetDevice(device));
     GRAB_CUDA(cudaDeviceGetAttribute(&ix.num_sms, cudaDevAttrMultiProcessorCount, device));
     GRAB_CUDA(cudaStreamCreateWithFlags(&ix.stream, cudaStreamNonBlocking));
+    {
+      // keep stream-ordered scratch (visited tables, staging) mapped across calls
+      cudaMemPool_t pool;
+      GRAB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      GRAB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     ix.dim = dim;
     ix.dp = (dim + 3) / 4 * 4;
     ix.n_cap = capacity;

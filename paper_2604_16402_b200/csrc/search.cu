@@ -10,14 +10,21 @@
 //               scalar pre-check before any distance, stamp, admit
 //   result      top_k + truncated flag 226-233
 //
-// B200 mapping: a persistent grid of warps, each owning one query at a time.
-// Query vector lives in registers (float4 per lane per 128-float chunk);
-// candidate rows are fetched with 16-byte ld.global.nc, G rows in flight per
-// lane, reduced with one fixed xor tree in f64 (parity with the reference's
-// f64 accumulation). Queue, candidate buffer, per-iteration dedup table and
-// the exact visited hash set live in shared memory; the visited set is
-// speculatively sized and a query that would exceed 3/4 load is re-run with
-// a table sized for the worst case (never a forgetful hash).
+// B200 mapping (v2): a persistent grid of warps, each owning one query at a
+// time, sized to fill every SM (>= 16 resident warps). Per-warp shared memory
+// holds only the queue (single buffer, merged in place), the candidate buffer
+// and the per-iteration dedup table (~7 KB at itopk 256). The exact visited set
+// lives in a per-warp global table (L2-resident, cleared by the owning warp at
+// query start) with CAS inserts issued for the whole iteration at once; a query
+// whose inserts would pass 3/4 load is re-run with a worst-case table (never a
+// forgetful hash, which would re-admit nodes and break parity). Each iteration
+// issues all adjacency loads, then all Attr{scalar, slot} loads, then all
+// visited CASes before consuming any, and candidate rows are fetched G at a
+// time with 16-byte ld.global.nc; every distance is reduced in f64 with the
+// library's one xor tree (bit-identical across kernels).
+#include <cstdio>
+#include <cstdlib>
+
 #include "index.cuh"
 #include "rng.cuh"
 #include "search.cuh"
@@ -44,96 +51,70 @@ void upload_pcg_jump_tables() {
 
 __device__ __forceinline__ uint32_t hash32(uint32_t k) { return k * 0x9E3779B1u; }
 
-// insert phys id into an open-addressing set of 2^lg entries (0 = empty).
-// Returns true when newly inserted.
+// Open-addressing set of 2^lg u32 entries (value key+1, 0 = empty).
+// Probe loops are written with a single structured exit: early returns from
+// inside a data-dependent loop make the warp look unconverged to the compiler
+// and turn every later shuffle into the slow collective fallback.
 __device__ __forceinline__ bool set_insert(uint32_t* tab, uint32_t lg, uint32_t key) {
-  uint32_t mask = (1u << lg) - 1;
+  const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
-  uint32_t v = key + 1;
-  while (true) {
-    uint32_t cur = atomicCAS(tab + h, 0u, v);
-    if (cur == 0u) return true;
-    if (cur == v) return false;
+  const uint32_t v = key + 1;
+  uint32_t cur = atomicCAS(tab + h, 0u, v);
+  while (cur != 0u && cur != v) {
     h = (h + 1) & mask;
+    cur = atomicCAS(tab + h, 0u, v);
   }
+  return cur == 0u;
 }
 
 __device__ __forceinline__ bool set_contains(const uint32_t* tab, uint32_t lg, uint32_t key) {
-  uint32_t mask = (1u << lg) - 1;
+  const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
-  uint32_t v = key + 1;
-  while (true) {
-    uint32_t cur = *((volatile const uint32_t*)(tab + h));
-    if (cur == v) return true;
-    if (cur == 0u) return false;
+  const uint32_t v = key + 1;
+  uint32_t cur = *((volatile const uint32_t*)(tab + h));
+  while (cur != 0u && cur != v) {
     h = (h + 1) & mask;
+    cur = *((volatile const uint32_t*)(tab + h));
   }
+  return cur == v;
 }
 
 __device__ __forceinline__ void clear_words(uint32_t* p, uint32_t n) {
   // n is a multiple of 128 (4 words per lane per step)
-  uint4 z = make_uint4(0, 0, 0, 0);
+  const uint4 z = make_uint4(0, 0, 0, 0);
   for (uint32_t i = lane_id() * 4; i < n; i += 128) *reinterpret_cast<uint4*>(p + i) = z;
 }
 
-struct WarpSmem {
-  double* qd[2];
-  uint32_t* qs[2];
-  uint32_t* qp[2];
-  uint8_t* qf[2];
-  double* cd;
-  uint32_t* cs;
-  uint32_t* cp;
-  uint32_t* dedup;
-  uint32_t* fr;
-  uint32_t* vis;
+// ---------------------------------------------------------------- layout
+__host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+struct WarpLayout {
+  uint32_t qd, qs, qp, qf, cd, cs, cp, dd, fr, bytes;
 };
 
-__host__ __device__ inline uint32_t align8(uint32_t x) { return (x + 7u) & ~7u; }
-
-__host__ __device__ inline uint32_t warp_smem_bytes(const SearchShape& s, bool vis_in_smem) {
-  uint32_t b = 0;
-  b += 2 * align8(s.itopk * 8);
-  b += 2 * align8(s.itopk * 4) * 2;
-  b += 2 * align8(s.itopk);
-  b += align8(s.cmax * 8) + 2 * align8(s.cmax * 4);
-  b += align8(s.dsz * 4);
-  b += align8(s.width * 4);
-  b = (b + 15u) & ~15u;
-  if (vis_in_smem) b += (1u << s.vlog2) * 4;
-  return b;
-}
-
-__device__ inline WarpSmem carve(uint8_t* base, const SearchShape& s) {
-  WarpSmem w;
-  uint8_t* p = base;
-  for (int i = 0; i < 2; ++i) {
-    w.qd[i] = (double*)p;
-    p += align8(s.itopk * 8);
-  }
-  for (int i = 0; i < 2; ++i) {
-    w.qs[i] = (uint32_t*)p;
-    p += align8(s.itopk * 4);
-    w.qp[i] = (uint32_t*)p;
-    p += align8(s.itopk * 4);
-  }
-  for (int i = 0; i < 2; ++i) {
-    w.qf[i] = p;
-    p += align8(s.itopk);
-  }
-  w.cd = (double*)p;
-  p += align8(s.cmax * 8);
-  w.cs = (uint32_t*)p;
-  p += align8(s.cmax * 4);
-  w.cp = (uint32_t*)p;
-  p += align8(s.cmax * 4);
-  w.dedup = (uint32_t*)p;
-  p += align8(s.dsz * 4);
-  w.fr = (uint32_t*)p;
-  p += align8(s.width * 4);
-  p = (uint8_t*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-  w.vis = (uint32_t*)p;
-  return w;
+__host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
+  WarpLayout l;
+  uint32_t o = 0;
+  l.qd = o;
+  o += align16(s.itopk * 8);
+  l.cd = o;
+  o += align16(s.cmax * 8);
+  l.qs = o;
+  o += align16(s.itopk * 4);
+  l.qp = o;
+  o += align16(s.itopk * 4);
+  l.cs = o;
+  o += align16(s.cmax * 4);
+  l.cp = o;
+  o += align16(s.cmax * 4);
+  l.dd = o;
+  o += align16(s.dsz * 4);
+  l.fr = o;
+  o += align16(s.width * 4);
+  l.qf = o;
+  o += align16(s.itopk);
+  l.bytes = o;
+  return l;
 }
 
 // ---------------------------------------------------------------- distances
@@ -146,7 +127,7 @@ template <int NC>
 __device__ __forceinline__ void load_query(QueryRegs<NC>& r, const float* q, uint32_t dp) {
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    uint32_t col = (c * 32 + lane_id()) * 4;
+    const uint32_t col = (c * 32 + lane_id()) * 4;
     r.q[c] = col < dp ? *reinterpret_cast<const float4*>(q + col) : make_float4(0, 0, 0, 0);
   }
 }
@@ -158,31 +139,35 @@ struct GroupOf {
 
 // Distances for cand[0..n): writes cd[i]. All lanes participate.
 template <int NC>
-__device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* X, uint32_t dp, const uint32_t* cp,
-                                      double* cd, uint32_t n) {
+__device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __restrict__ X, uint32_t dp,
+                                      const uint32_t* cp, double* cd, uint32_t n) {
   constexpr int G = GroupOf<NC>::G;
   const uint32_t lane = lane_id();
   for (uint32_t base = 0; base < n; base += G) {
     float4 x[G][NC];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      uint32_t i = base + g;
-      uint32_t p = i < n ? cp[i] : cp[0];
+      const uint32_t i = base + g;
+      const uint32_t p = cp[i < n ? i : base];
       const float* row = X + (uint64_t)p * dp;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        uint32_t col = (c * 32 + lane) * 4;
+        const uint32_t col = (c * 32 + lane) * 4;
         x[g][c] = col < dp ? ldg_nc_f4(row + col) : make_float4(0, 0, 0, 0);
       }
     }
+    double part[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       double acc = 0.0;
 #pragma unroll
       for (int c = 0; c < NC; ++c) acc = sq4(x[g][c], qr.q[c], acc);
-      acc = warp_sum(acc);
-      if (lane == 0 && base + g < n) cd[base + g] = acc;
+      part[g] = acc;
     }
+    const double v = reduce_scatter<G>(part);
+    constexpr uint32_t SPAN = 32 / G;  // lanes holding each candidate's sum
+    const uint32_t g = lane / SPAN;
+    if ((lane % SPAN) == 0 && base + g < n) cd[base + g] = v;
   }
   __syncwarp();
 }
@@ -199,18 +184,17 @@ __device__ __forceinline__ void bitonic_sort(double* d, uint32_t* s, uint32_t* p
   for (uint32_t k = 2; k <= P; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       for (uint32_t i = lane; i < P; i += 32) {
-        uint32_t l = i ^ j;
+        const uint32_t l = i ^ j;
         if (l > i) {
-          double di = d[i], dl = d[l];
-          uint32_t si = s[i], sl = s[l];
-          bool asc = (i & k) == 0;
-          bool gt = key_less(dl, sl, di, si);  // element i > element l
-          if (gt == asc) {
+          const double di = d[i], dl = d[l];
+          const uint32_t si = s[i], sl = s[l];
+          const bool asc = (i & k) == 0;
+          if (key_less(dl, sl, di, si) == asc) {
             d[i] = dl;
             d[l] = di;
             s[i] = sl;
             s[l] = si;
-            uint32_t t = p[i];
+            const uint32_t t = p[i];
             p[i] = p[l];
             p[l] = t;
           }
@@ -225,7 +209,7 @@ __device__ __forceinline__ void bitonic_sort(double* d, uint32_t* s, uint32_t* p
 __device__ __forceinline__ uint32_t rank_in(const double* d, const uint32_t* s, uint32_t n, double kd, uint32_t ks) {
   uint32_t lo = 0, hi = n;
   while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
+    const uint32_t mid = (lo + hi) >> 1;
     if (key_less(d[mid], s[mid], kd, ks))
       lo = mid + 1;
     else
@@ -234,35 +218,33 @@ __device__ __forceinline__ uint32_t rank_in(const double* d, const uint32_t* s, 
   return lo;
 }
 
-// Admit cand[0..nc) into queue buffer `cur` of length L (CandidateQueue.admit).
-// Returns new length; flips `cur`.
-__device__ uint32_t admit(WarpSmem& w, int& cur, uint32_t L, uint32_t nc, uint32_t itopk) {
+// CandidateQueue.admit: merge cand[0..nc) into the queue (length L) in place,
+// truncated to itopk. Returns the new length.
+__device__ __forceinline__ uint32_t admit(double* qd, uint32_t* qs, uint32_t* qp, uint8_t* qf, double* cd,
+                                          uint32_t* cs, uint32_t* cp, uint32_t L, uint32_t nc, uint32_t itopk) {
   const uint32_t lane = lane_id();
-  double* qd = w.qd[cur];
-  uint32_t* qs = w.qs[cur];
-  // candidates that cannot survive truncation are dropped up front
-  if (L == itopk && nc) {
-    double td = qd[L - 1];
-    uint32_t ts = qs[L - 1];
+  if (L == itopk && nc) {  // candidates that cannot survive truncation are dropped up front
+    const double td = qd[L - 1];
+    const uint32_t ts = qs[L - 1];
     uint32_t kept = 0;
     for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
-      uint32_t i = b0 + lane;
+      const uint32_t i = b0 + lane;
       bool ok = false;
       double d = 0;
       uint32_t s = 0, p = 0;
       if (i < nc) {
-        d = w.cd[i];
-        s = w.cs[i];
-        p = w.cp[i];
+        d = cd[i];
+        s = cs[i];
+        p = cp[i];
         ok = key_less(d, s, td, ts);
       }
-      uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
       __syncwarp();
       if (ok) {
-        uint32_t pos = kept + __popc(m & ((1u << lane) - 1));
-        w.cd[pos] = d;
-        w.cs[pos] = s;
-        w.cp[pos] = p;
+        const uint32_t pos = kept + __popc(m & ((1u << lane) - 1));
+        cd[pos] = d;
+        cs[pos] = s;
+        cp[pos] = p;
       }
       kept += __popc(m);
       __syncwarp();
@@ -272,57 +254,68 @@ __device__ uint32_t admit(WarpSmem& w, int& cur, uint32_t L, uint32_t nc, uint32
   if (nc == 0) return L;
   uint32_t P = 32;
   while (P < nc) P <<= 1;
-  bitonic_sort(w.cd, w.cs, w.cp, nc, P);
-  int nxt = cur ^ 1;
-  double* od = w.qd[nxt];
-  uint32_t* os = w.qs[nxt];
-  uint32_t* op = w.qp[nxt];
-  uint8_t* of = w.qf[nxt];
-  for (uint32_t i = lane; i < L; i += 32) {
-    uint32_t pos = i + rank_in(w.cd, w.cs, nc, qd[i], qs[i]);
-    if (pos < itopk) {
-      od[pos] = qd[i];
-      os[pos] = qs[i];
-      op[pos] = w.qp[cur][i];
-      of[pos] = w.qf[cur][i];
-    }
+  bitonic_sort(cd, cs, cp, nc, P);
+  // candidate destinations against the OLD queue (<= 4 per lane, cmax <= 128 on this path)
+  uint32_t cpos[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t j = lane + 32 * t;
+    cpos[t] = j < nc ? j + rank_in(qd, qs, L, cd[j], cs[j]) : 0xFFFFFFFFu;
   }
-  for (uint32_t j = lane; j < nc; j += 32) {
-    uint32_t pos = j + rank_in(qd, qs, L, w.cd[j], w.cs[j]);
+  // move queue entries, highest chunk first (destinations are >= sources)
+  for (int32_t b0 = (int32_t)((L - 1) & ~31u); b0 >= 0; b0 -= 32) {
+    const uint32_t i = (uint32_t)b0 + lane;
+    double d = 0;
+    uint32_t s = 0, p = 0, pos = 0xFFFFFFFFu;
+    uint8_t f = 0;
+    if (i < L) {
+      d = qd[i];
+      s = qs[i];
+      p = qp[i];
+      f = qf[i];
+      pos = i + rank_in(cd, cs, nc, d, s);
+    }
+    __syncwarp();
     if (pos < itopk) {
-      od[pos] = w.cd[j];
-      os[pos] = w.cs[j];
-      op[pos] = w.cp[j];
-      of[pos] = 0;
+      qd[pos] = d;
+      qs[pos] = s;
+      qp[pos] = p;
+      qf[pos] = f;
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t j = lane + 32 * t;
+    if (cpos[t] < itopk) {
+      qd[cpos[t]] = cd[j];
+      qs[cpos[t]] = cs[j];
+      qp[cpos[t]] = cp[j];
+      qf[cpos[t]] = 0;
     }
   }
   __syncwarp();
-  cur = nxt;
   return min(itopk, L + nc);
 }
 
 // ---------------------------------------------------------------- seeds
-struct SeedOut {
-  uint32_t n;         // seeds written to cand[0..n)
-  uint32_t attempts;  // draws requested (SearchStats.seed_attempts)
-};
-
 // _sample_seeds (searcher.py:101-153). Draws of one jump-ahead round (64 words,
 // lane L owns output 32r+L = words lo,hi) are compacted into `stage` in word
-// order, then consumed 32 at a time in draw order.
-__device__ SeedOut sample_seeds(const SearchArgs& a, WarpSmem& w, uint32_t lo_b, uint32_t hi_b, float lo_f,
-                                float hi_f, uint64_t rng_seed, uint32_t vlg) {
+// order, then consumed 32 at a time in draw order. Returns seeds written to
+// (cp, cs)[0..n); *attempts = SearchStats.seed_attempts.
+__device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t* cp, uint32_t* cs, uint32_t* vis,
+                                 uint32_t vlg, uint32_t lo_b, uint32_t hi_b, float lo_f, float hi_f,
+                                 uint64_t rng_seed, uint32_t* attempts) {
   const uint32_t lane = lane_id();
   const uint32_t lt = (1u << lane) - 1;
   const uint32_t want = a.want;
-  uint32_t* stage = w.dedup;  // >= 128 words, idle during seeding
-  SeedOut r{0, 0};
   const uint64_t c0 = a.bcum[lo_b];
   const uint64_t total = a.bcum[hi_b + 1] - c0;
   uint32_t picked = 0;
+  *attempts = 0;
   if (total > 0) {
     const uint32_t ndraw = 4 * want;
-    r.attempts = ndraw;
+    *attempts = ndraw;
     const uint32_t tot = (uint32_t)total;
     const uint32_t thresh = (0u - tot) % tot;
     const Pcg64 g = pcg64_from_seed(rng_seed);
@@ -356,7 +349,7 @@ __device__ SeedOut sample_seeds(const SearchArgs& a, WarpSmem& w, uint32_t lo_b,
           const uint64_t f = c0 + stage[off + lane];
           uint32_t lo = lo_b, hi = hi_b;  // bucket b with bcum[b] <= f < bcum[b+1]
           while (lo < hi) {
-            uint32_t mid = (lo + hi + 1) >> 1;
+            const uint32_t mid = (lo + hi + 1) >> 1;
             if (__ldg(a.bcum + mid) <= f)
               lo = mid;
             else
@@ -370,14 +363,14 @@ __device__ SeedOut sample_seeds(const SearchArgs& a, WarpSmem& w, uint32_t lo_b,
         const bool inr = have && slot < a.n_live && sv >= lo_f && sv <= hi_f;
         const uint32_t same = __match_any_sync(0xFFFFFFFFu, inr ? phys : 0xFFFFFFFFu);
         const bool first = inr && (uint32_t)(__ffs(same) - 1) == lane;
-        const bool fresh = first && !set_contains(w.vis, vlg, phys);
+        const bool fresh = first && !set_contains(vis, vlg, phys);
         const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fresh);
         const uint32_t rank = __popc(fm & lt);
         const bool take = fresh && rank < want - picked;
         if (take) {
-          set_insert(w.vis, vlg, phys);
-          w.cp[picked + rank] = phys;
-          w.cs[picked + rank] = slot;
+          set_insert(vis, vlg, phys);
+          cp[picked + rank] = phys;
+          cs[picked + rank] = slot;
         }
         picked += __popc(__ballot_sync(0xFFFFFFFFu, take));
         drawn += navail;
@@ -400,145 +393,176 @@ __device__ SeedOut sample_seeds(const SearchArgs& a, WarpSmem& w, uint32_t lo_b,
         if (i < cnt) {
           const Attr at = ld_attr(a.attr, phys);
           slot = at.slot;
-          ok = slot < a.n_live && at.s >= lo_f && at.s <= hi_f && !set_contains(w.vis, vlg, phys);
+          ok = slot < a.n_live && at.s >= lo_f && at.s <= hi_f && !set_contains(vis, vlg, phys);
         }
         const uint32_t msk = __ballot_sync(0xFFFFFFFFu, ok);
         const uint32_t rank = __popc(msk & lt);
         const bool take = ok && rank < want - picked;
         if (take) {
-          set_insert(w.vis, vlg, phys);
-          w.cp[picked + rank] = phys;
-          w.cs[picked + rank] = slot;
+          set_insert(vis, vlg, phys);
+          cp[picked + rank] = phys;
+          cs[picked + rank] = slot;
         }
         picked += __popc(__ballot_sync(0xFFFFFFFFu, take));
         __syncwarp();
       }
     }
   }
-  r.n = picked;
-  return r;
+  return picked;
 }
 
 // ---------------------------------------------------------------- kernel
-template <int NC>
-__global__ void __launch_bounds__(128) k_search(SearchArgs a, SearchShape sh) {
+// NC: 128-float chunks per row; EPL: gathered neighbours per lane per iteration
+// (width * K_max <= 32 * EPL).
+#ifndef GRAB_SEARCH_MINB
+#define GRAB_SEARCH_MINB 6  // 6 blocks x 4 warps: 85 registers (small spills beat 4 blocks)
+#endif
+template <int NC, int EPL>
+__global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, SearchShape sh) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t wpb = blockDim.x >> 5;
-  const bool vis_smem = a.gtab == nullptr;
-  const uint32_t wbytes = warp_smem_bytes(sh, vis_smem);
-  WarpSmem w = carve(smem + wib * wbytes, sh);
+  const WarpLayout lay = warp_layout(sh);
+  uint8_t* base = smem + wib * lay.bytes;
+  double* qd = (double*)(base + lay.qd);
+  uint32_t* qs = (uint32_t*)(base + lay.qs);
+  uint32_t* qp = (uint32_t*)(base + lay.qp);
+  uint8_t* qf = base + lay.qf;
+  double* cd = (double*)(base + lay.cd);
+  uint32_t* cs = (uint32_t*)(base + lay.cs);
+  uint32_t* cp = (uint32_t*)(base + lay.cp);
+  uint32_t* dd = (uint32_t*)(base + lay.dd);
+  uint32_t* fr = (uint32_t*)(base + lay.fr);
   const uint32_t gw = blockIdx.x * wpb + wib;
-  if (!vis_smem) w.vis = a.gtab + (uint64_t)gw * (1u << sh.vlog2);
   const uint32_t vlg = sh.vlog2;
+  uint32_t* vis = a.gtab + ((uint64_t)gw << vlg);
   const uint32_t vcap = (1u << vlg) / 4 * 3;
   const uint32_t nw = gridDim.x * wpb;
+  const uint32_t dlg = 31 - __clz(sh.dsz);
+  const uint32_t K = a.k_max;
 
   for (uint32_t item = gw; item < a.nwork; item += nw) {
     const uint32_t qi = a.qmap ? a.qmap[item] : item;
-    const double lo_d = a.lower[(uint64_t)qi * a.range_stride];
-    const double hi_d = a.upper[(uint64_t)qi * a.range_stride];
-    const float lo_f = __double2float_rn(lo_d), hi_f = __double2float_rn(hi_d);
+    const float lo_f = __double2float_rn(a.lower[(uint64_t)qi * a.range_stride]);
+    const float hi_f = __double2float_rn(a.upper[(uint64_t)qi * a.range_stride]);
     grab_search_stats st = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t L = 0;
-    int cur = 0;
     bool overflow = false;
     if (a.n_live > 0 && a.m > 0) {
-      clear_words(w.vis, 1u << vlg);
+      clear_words(vis, 1u << vlg);
       __syncwarp();
       QueryRegs<NC> qr;
       load_query<NC>(qr, a.qphys ? a.X + (uint64_t)a.qphys[qi] * a.dp : a.Q + (uint64_t)qi * a.dp, a.dp);
       const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f);
       const uint32_t hi_b = bucket_of_f32(a.bound, a.m, hi_f);
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
-      SeedOut so = sample_seeds(a, w, lo_b, hi_b, lo_f, hi_f, seed, vlg);
-      st.seed_attempts = so.attempts;
-      uint32_t vis_n = so.n;
-      if (so.n > 0) {
-        score<NC>(qr, a.X, a.dp, w.cp, w.cd, so.n);
-        st.dist_evals = st.seed_evals = so.n;
-        L = admit(w, cur, 0, so.n, sh.itopk);
-        const uint32_t fan = sh.width * a.k_max;
+      uint32_t attempts = 0;
+      const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, vlg, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
+      st.seed_attempts = attempts;
+      uint32_t vis_n = ns;
+      if (ns > 0) {
+        score<NC>(qr, a.X, a.dp, cp, cd, ns);
+        st.dist_evals = st.seed_evals = ns;
+        L = admit(qd, qs, qp, qf, cd, cs, cp, 0, ns, sh.itopk);
         for (uint32_t it = 0; it < a.max_iter; ++it) {
           // frontier: first `width` unexpanded entries
           uint32_t nf = 0;
           for (uint32_t b0 = 0; b0 < L && nf < sh.width; b0 += 32) {
-            uint32_t i = b0 + lane;
-            bool un = i < L && w.qf[cur][i] == 0;
-            uint32_t m = __ballot_sync(0xFFFFFFFFu, un);
-            uint32_t rank = __popc(m & ((1u << lane) - 1));
+            const uint32_t i = b0 + lane;
+            const bool un = i < L && qf[i] == 0;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, un);
+            const uint32_t rank = __popc(m & ((1u << lane) - 1));
             if (un && nf + rank < sh.width) {
-              w.fr[nf + rank] = w.qp[cur][i];
-              w.qf[cur][i] = 1;
+              fr[nf + rank] = qp[i];
+              qf[i] = 1;
             }
             nf = min(sh.width, nf + __popc(m));
           }
           __syncwarp();
           if (nf == 0) break;
-          if (vis_n + nf * a.k_max > vcap) {
+          const uint32_t fan = nf * K;
+          if (vis_n + fan > vcap) {
             overflow = true;
             break;
           }
           st.iterations++;
           st.expanded += nf;
-          // gather, dedup, pre-check, visited
-          clear_words(w.dedup, sh.dsz);
-          __syncwarp();
-          const uint32_t dlg = 31 - __clz(sh.dsz);
-          uint32_t nc = 0;
-          for (uint32_t b0 = 0; b0 < nf * a.k_max; b0 += 32) {
-            uint32_t e = b0 + lane;
-            bool cand = false, uniq = false, rej = false;
-            uint32_t v = kSentinel, slot = 0;
-            if (e < nf * a.k_max) {
-              uint32_t row = w.fr[e / a.k_max];
-              v = __ldg(a.adj + (uint64_t)row * a.k_max + (e % a.k_max));
-              if (v != kSentinel) {
-                Attr at = ld_attr(a.attr, v);
-                slot = at.slot;
-                if (slot < a.n_live) {
-                  uniq = set_insert(w.dedup, dlg, v);
-                  if (uniq) {
-                    bool inr = at.s >= lo_f && at.s <= hi_f;
-                    rej = !inr;
-                    if (inr) cand = set_insert(w.vis, vlg, v);
-                  }
-                }
-              }
+          clear_words(dd, sh.dsz);
+          // (1) all adjacency entries of the frontier rows
+          uint32_t v[EPL];
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) {
+            const uint32_t e = lane + 32 * t;
+            v[t] = kSentinel;
+            if (e < fan) v[t] = __ldg(a.adj + (uint64_t)fr[e / K] * K + (e % K));
+          }
+          // (2) all Attr{scalar, slot}
+          float sv[EPL];
+          uint32_t sl[EPL];
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) {
+            sl[t] = kNoSlot;
+            sv[t] = 0.f;
+            if (v[t] != kSentinel) {
+              const Attr at = ld_attr(a.attr, v[t]);
+              sl[t] = at.slot;
+              sv[t] = at.s;
             }
-            uint32_t cm = __ballot_sync(0xFFFFFFFFu, cand);
-            st.gathered += __popc(__ballot_sync(0xFFFFFFFFu, uniq));
-            st.precheck_rejected += __popc(__ballot_sync(0xFFFFFFFFu, rej));
-            if (cand) {
-              uint32_t pos = nc + __popc(cm & ((1u << lane) - 1));
-              w.cp[pos] = v;
-              w.cs[pos] = slot;
+          }
+          __syncwarp();
+          // (3) per-iteration unique (shared), pre-check, (4) visited CAS (global)
+          uint32_t uniq_bits = 0, cand_bits = 0, rej_bits = 0;
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) {
+            if (sl[t] < a.n_live && set_insert(dd, dlg, v[t])) {
+              uniq_bits |= 1u << t;
+              if (sv[t] >= lo_f && sv[t] <= hi_f)
+                cand_bits |= 1u << t;
+              else
+                rej_bits |= 1u << t;
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < EPL; ++t)
+            if (((cand_bits >> t) & 1u) && !set_insert(vis, vlg, v[t])) cand_bits &= ~(1u << t);
+          // (5) compact candidates in gather order + stats
+          uint32_t nc = 0;
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) {
+            const bool c = (cand_bits >> t) & 1u;
+            const uint32_t cm = __ballot_sync(0xFFFFFFFFu, c);
+            st.gathered += __popc(__ballot_sync(0xFFFFFFFFu, (uniq_bits >> t) & 1u));
+            st.precheck_rejected += __popc(__ballot_sync(0xFFFFFFFFu, (rej_bits >> t) & 1u));
+            if (c) {
+              const uint32_t pos = nc + __popc(cm & ((1u << lane) - 1));
+              cp[pos] = v[t];
+              cs[pos] = sl[t];
             }
             nc += __popc(cm);
           }
-          (void)fan;
           __syncwarp();
           vis_n += nc;
           if (nc == 0) continue;
           st.in_range_new += nc;
           st.dist_evals += nc;
-          score<NC>(qr, a.X, a.dp, w.cp, w.cd, nc);
-          L = admit(w, cur, L, nc, sh.itopk);
+          score<NC>(qr, a.X, a.dp, cp, cd, nc);
+          L = admit(qd, qs, qp, qf, cd, cs, cp, L, nc, sh.itopk);
         }
       }
     }
     if (overflow) {
       if (lane == 0) {
-        uint32_t pos = atomicAdd(a.ovf_count, 1u);
+        const uint32_t pos = atomicAdd(a.ovf_count, 1u);
         a.ovf_list[pos] = qi;
       }
+      __syncwarp();
       continue;
     }
     const uint32_t cnt = min(L, a.k);
     for (uint32_t i = lane; i < a.k; i += 32) {
-      a.out_slots[(uint64_t)qi * a.k + i] = i < cnt ? (int64_t)w.qs[cur][i] : -1;
-      a.out_dists[(uint64_t)qi * a.k + i] = i < cnt ? w.qd[cur][i] : __longlong_as_double(0x7FF8000000000000ll);
+      a.out_slots[(uint64_t)qi * a.k + i] = i < cnt ? (int64_t)qs[i] : -1;
+      a.out_dists[(uint64_t)qi * a.k + i] = i < cnt ? qd[i] : __longlong_as_double(0x7FF8000000000000ll);
     }
     if (lane == 0) {
       a.out_counts[qi] = cnt;
@@ -555,100 +579,120 @@ static uint32_t ceil_log2(uint64_t x) {
   return l;
 }
 
-static void launch(const SearchArgs& a, const SearchShape& sh, int num_sms, cudaStream_t st, uint32_t* gtab_ws,
-                   uint32_t nwarps_cap) {
-  const bool vis_smem = a.gtab == nullptr;
-  const uint32_t wbytes = warp_smem_bytes(sh, vis_smem);
-  uint32_t wpb = 4;
-  while (wpb > 1 && wbytes * wpb > 200 * 1024) wpb >>= 1;
-  const uint32_t smem = wbytes * wpb;
-  if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "search parameters exceed shared memory (itopk too large)");
-  uint32_t nc_chunks = (uint32_t)div_up(a.dp, 128);
-  auto go = [&](auto kern) {
-    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
-    per_sm = per_sm < 1 ? 1 : per_sm;
-    uint64_t blocks = div_up(a.nwork, wpb);
-    uint64_t cap = (uint64_t)per_sm * num_sms;
-    if (nwarps_cap) cap = std::min<uint64_t>(cap, div_up(nwarps_cap, wpb));
-    blocks = std::min(blocks, cap);
-    if (blocks == 0) return;
-    kern<<<(unsigned)blocks, 32 * wpb, smem, st>>>(a, sh);
-    GRAB_CHECK_LAUNCH();
-  };
-  if (nc_chunks <= 1)
-    go(k_search<1>);
-  else if (nc_chunks <= 2)
-    go(k_search<2>);
-  else if (nc_chunks <= 4)
-    go(k_search<4>);
-  else if (nc_chunks <= 8)
-    go(k_search<8>);
-  else
-    throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported by the search kernel");
-  (void)gtab_ws;
-}
-
 SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst) {
   SearchShape s;
   s.itopk = itopk;
   s.width = width;
-  uint32_t fan = width * k_max;
+  const uint32_t fan = width * k_max;
   s.cmax = 1u << ceil_log2(std::max<uint64_t>(std::max(fan, want), 32));  // bitonic pads to a power of 2
   s.dsz = 1u << ceil_log2(std::max<uint64_t>(2ull * fan, 128));
   if (!worst) {
-    s.vlog2 = std::min<uint32_t>(14, std::max<uint32_t>(11, ceil_log2((uint64_t)itopk * 24)));
+    s.vlog2 = std::min<uint32_t>(15, std::max<uint32_t>(11, ceil_log2((uint64_t)itopk * 24)));
   } else {
-    uint64_t bound = (uint64_t)want + (uint64_t)max_iter * fan + fan;
+    const uint64_t bound = (uint64_t)want + (uint64_t)max_iter * fan + fan;
     s.vlog2 = std::max<uint32_t>(11, ceil_log2(bound * 4 / 3 + 1));
   }
   return s;
 }
 
+// returns the number of warps the grid runs (for sizing the visited tables)
+template <int NC, int EPL>
+static void launch_t(const SearchArgs& a, const SearchShape& sh, uint32_t wpb, uint32_t blocks, uint32_t smem,
+                     cudaStream_t st) {
+  auto kern = k_search<NC, EPL>;
+  GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<blocks, 32 * wpb, smem, st>>>(a, sh);
+  GRAB_CHECK_LAUNCH();
+}
+
+template <int NC>
+static void dispatch_epl(uint32_t epl, const SearchArgs& a, const SearchShape& sh, uint32_t wpb, uint32_t blocks,
+                         uint32_t smem, cudaStream_t st) {
+  if (epl <= 1)
+    launch_t<NC, 1>(a, sh, wpb, blocks, smem, st);
+  else if (epl <= 2)
+    launch_t<NC, 2>(a, sh, wpb, blocks, smem, st);
+  else if (epl <= 4)
+    launch_t<NC, 4>(a, sh, wpb, blocks, smem, st);
+  else
+    throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
+}
+
+static int occupancy_blocks(uint32_t nc, uint32_t epl, uint32_t wpb, uint32_t smem) {
+  int per_sm = 0;
+  auto q = [&](auto kern) {
+    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
+  };
+  // occupancy depends on registers (template) and smem; probe the instance that will run
+#define GRAB_Q(NC_, EPL_) \
+  if (nc == NC_ && epl == EPL_) q(k_search<NC_, EPL_>);
+  GRAB_Q(1, 1) GRAB_Q(1, 2) GRAB_Q(1, 4) GRAB_Q(2, 1) GRAB_Q(2, 2) GRAB_Q(2, 4) GRAB_Q(4, 1) GRAB_Q(4, 2)
+  GRAB_Q(4, 4) GRAB_Q(8, 1) GRAB_Q(8, 2) GRAB_Q(8, 4)
+#undef GRAB_Q
+  return per_sm < 1 ? 1 : per_sm;
+}
+
+static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_t st, DBufLite& tables) {
+  const WarpLayout lay = warp_layout(sh);
+  const uint32_t wpb = 4;
+  const uint32_t smem = lay.bytes * wpb;
+  if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "search parameters exceed shared memory (itopk too large)");
+  uint32_t nc = (uint32_t)div_up(a.dp, 128);
+  nc = nc <= 1 ? 1 : nc <= 2 ? 2 : nc <= 4 ? 4 : nc <= 8 ? 8 : 0;
+  if (!nc) throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported by the search kernel");
+  uint32_t epl = (uint32_t)div_up(sh.width * a.k_max, 32);
+  epl = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
+  if (epl > 4 || sh.cmax > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
+  const int per_sm = occupancy_blocks(nc, epl, wpb, smem);
+  const uint64_t blocks = std::min<uint64_t>(div_up(a.nwork, wpb), (uint64_t)per_sm * num_sms);
+  if (!blocks) return;
+  // one visited table per resident warp
+  const uint64_t words = blocks * wpb * (1ull << sh.vlog2);
+  tables.ensure(words * 4, st);
+  a.gtab = (uint32_t*)tables.p;
+  if (nc == 1)
+    dispatch_epl<1>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
+  else if (nc == 2)
+    dispatch_epl<2>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
+  else if (nc == 4)
+    dispatch_epl<4>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
+  else
+    dispatch_epl<8>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
+}
+
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
+  if (a.width * a.k_max > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
   SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false);
-  uint32_t* ovf;
-  GRAB_CUDA(cudaMallocAsync(&ovf, (a.nwork + 1) * sizeof(uint32_t), st));
+  DBufLite tables, ovfb;
+  ovfb.ensure((a.nwork + 1) * sizeof(uint32_t), st);
+  uint32_t* ovf = (uint32_t*)ovfb.p;
   GRAB_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
   a.ovf_count = ovf;
   a.ovf_list = ovf + 1;
-  a.gtab = nullptr;
   a.qmap = nullptr;
-  launch(a, sh, ix.num_sms, st, nullptr, 0);
+  launch(a, sh, ix.num_sms, st, tables);
   uint32_t n_ovf = 0;
   GRAB_CUDA(cudaMemcpyAsync(&n_ovf, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   GRAB_CUDA(cudaStreamSynchronize(st));
+  if (getenv("GRAB_DEBUG")) fprintf(stderr, "[grab] search nwork=%u vlog2=%u overflow=%u\n", a.nwork, sh.vlog2, n_ovf);
   if (n_ovf) {
     // exact re-run of the overflowed queries with a worst-case visited table
     SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true);
     SearchArgs b = a;
-    uint32_t* qmap;
-    GRAB_CUDA(cudaMallocAsync(&qmap, n_ovf * sizeof(uint32_t), st));
-    GRAB_CUDA(cudaMemcpyAsync(qmap, a.ovf_list, n_ovf * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-    b.qmap = qmap;
+    DBufLite qm;
+    qm.ensure(n_ovf * sizeof(uint32_t), st);
+    GRAB_CUDA(cudaMemcpyAsync(qm.p, a.ovf_list, n_ovf * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    b.qmap = (const uint32_t*)qm.p;
     b.nwork = n_ovf;
     GRAB_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
-    uint32_t nwarps = std::min<uint32_t>(n_ovf, 4u * (uint32_t)ix.num_sms);
-    uint32_t* gtab = nullptr;
-    if (warp_smem_bytes(big, true) > 200 * 1024) {
-      uint64_t nwords = (uint64_t)nwarps * 4 * (1ull << big.vlog2);
-      GRAB_CUDA(cudaMallocAsync(&gtab, nwords * 4, st));
-      b.gtab = gtab;
-    }
-    launch(b, big, ix.num_sms, st, gtab, b.gtab ? nwarps : 0);
+    launch(b, big, ix.num_sms, st, tables);
     uint32_t again = 0;
     GRAB_CUDA(cudaMemcpyAsync(&again, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     GRAB_CUDA(cudaStreamSynchronize(st));
-    if (gtab) cudaFreeAsync(gtab, st);
-    cudaFreeAsync(qmap, st);
-    if (again) {
-      cudaFreeAsync(ovf, st);
-      throw Error(GRAB_ERR_CUDA, "visited-set overflow persisted on the worst-case retry");
-    }
+    if (again) throw Error(GRAB_ERR_CUDA, "visited-set overflow persisted on the worst-case retry");
   }
-  GRAB_CUDA(cudaFreeAsync(ovf, st));
 }
 
 }  // namespace grab

@@ -1,0 +1,13 @@
+#!/bin/bash
+# Rebuild the search kernel with different register caps and time cfg2 search.
+cd "$(dirname "$0")/.."
+C=paper_2604_16402_b200/csrc
+make -C $C -j16 >/dev/null
+for MB in ${MINBS:-4 5 6}; do
+  (cd $C && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+     --expt-relaxed-constexpr -DGRAB_SEARCH_MINB=$MB -c search.cu -o build/search.o && \
+   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../libgrab.so $(ls *.cu | sed 's/\.cu$/.o/; s/^/build\//'))
+  echo "MINB=$MB"
+  python tools/profile_search.py --config cfg2 --reps 5 --time --points "${POINTS:-128:4:50,256:4:100}" 2>&1 | tail -2
+done
+touch $C/search.cu
