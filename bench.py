@@ -34,7 +34,7 @@ PRESETS = {
     "cfg3": dict(n=1_000_000, dim=960, cap=10_000, nq=10_000, sel=0.10),
 }
 GRID = [(32, 1, 50), (32, 2, 50), (48, 2, 50), (64, 2, 50), (64, 4, 50), (96, 4, 50), (128, 4, 50), (192, 4, 50),
-        (256, 4, 100)]
+        (128, 4, 100), (160, 4, 100), (192, 4, 100), (224, 4, 100), (256, 4, 100), (192, 2, 100), (256, 2, 150)]
 
 
 def env_int(k, d):

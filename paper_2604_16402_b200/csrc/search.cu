@@ -523,9 +523,26 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
                 rej_bits |= 1u << t;
             }
           }
+          {
+            // issue every first-probe CAS of the iteration before consuming any
+            const uint32_t vmask = (1u << vlg) - 1;
+            uint32_t h[EPL], cur[EPL];
 #pragma unroll
-          for (int t = 0; t < EPL; ++t)
-            if (((cand_bits >> t) & 1u) && !set_insert(vis, vlg, v[t])) cand_bits &= ~(1u << t);
+            for (int t = 0; t < EPL; ++t) {
+              h[t] = hash32(v[t]) >> (32 - vlg);
+              cur[t] = ((cand_bits >> t) & 1u) ? atomicCAS(vis + h[t], 0u, v[t] + 1) : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) {
+              if ((cand_bits >> t) & 1u) {
+                while (cur[t] != 0u && cur[t] != v[t] + 1) {  // rare collision: probe on
+                  h[t] = (h[t] + 1) & vmask;
+                  cur[t] = atomicCAS(vis + h[t], 0u, v[t] + 1);
+                }
+                if (cur[t] != 0u) cand_bits &= ~(1u << t);
+              }
+            }
+          }
           // (5) compact candidates in gather order + stats
           uint32_t nc = 0;
 #pragma unroll
