@@ -211,12 +211,16 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
   KnnJob* dj;
   GRAB_CUDA(cudaMallocAsync(&dj, jobs.size() * sizeof(KnnJob), st));
   GRAB_CUDA(cudaMemcpyAsync(dj, jobs.data(), jobs.size() * sizeof(KnnJob), cudaMemcpyHostToDevice, st));
-  size_t smem = (size_t)BK * (BM + 4) * 4 + (size_t)BK * (BN + 4) * 4 + (size_t)BM * (BN + 1) * 4 +
-                (size_t)BM * KP * 8;
-  if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "k too large for the kNN screen");
-  GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_knn_screen<<<(unsigned)jobs.size(), 256, smem, st>>>(dj, ix.X, ix.attr, norms, ix.dp, KP, cand, causal);
-  GRAB_CHECK_LAUNCH();
+  if (knn_tc_supported(ix, KP)) {
+    knn_screen_tc(ix, norms, dj, (uint32_t)jobs.size(), KP, cand, causal, st);
+  } else {
+    size_t smem = (size_t)BK * (BM + 4) * 4 + (size_t)BK * (BN + 4) * 4 + (size_t)BM * (BN + 1) * 4 +
+                  (size_t)BM * KP * 8;
+    if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "k too large for the kNN screen");
+    GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_knn_screen<<<(unsigned)jobs.size(), 256, smem, st>>>(dj, ix.X, ix.attr, norms, ix.dp, KP, cand, causal);
+    GRAB_CHECK_LAUNCH();
+  }
   // rerank every row touched by a job
   std::vector<uint32_t> rows;
   for (const KnnJob& j : jobs)

@@ -24,4 +24,10 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
                 uint32_t* out_ids, double* out_d, cudaStream_t st, bool causal = false);
 void row_norms(const DevIndex& ix, float* out, cudaStream_t st);
 
+// tcgen05 split-BF16 screen (knn_tc.cu): same output contract as the SIMT screen
+// (per query row, KP candidate phys ids in cand[row * KP ..]).
+bool knn_tc_supported(const DevIndex& ix, uint32_t KP);
+void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, uint32_t njobs, uint32_t KP,
+                   uint32_t* cand, bool causal, cudaStream_t st);
+
 }  // namespace grab

@@ -1,0 +1,369 @@
+// kNN screen on the 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Reference: pairwise_sq_dists + topk_ids_by_distance (builder.py:79-113) --
+// the build's only dense contraction (pass-1 buckets, the global graph and the
+// insert's in-bucket candidates all go through knn_device()).
+//
+// dot(a, b) is computed as a split-BF16 product: x = hi + lo with
+// hi = bf16(x), lo = bf16(x - hi); a.b ~= ah.bh + ah.bl + al.bh (three UMMAs
+// into one fp32 TMEM accumulator) -- relative error ~1e-5, far below the gap
+// between a row's k-th and (k+16)-th neighbour, and every survivor is
+// re-ranked exactly in f64 afterwards (knn.cu k_knn_rerank).
+//
+// CTA = one 128-row query tile x a stream of 64-row candidate tiles:
+//   warp 0    TMA producer (A hi/lo once, B hi/lo through a 3-stage ring)
+//   warp 1    TMEM allocator + single-thread UMMA issuer
+//             (kind::f16, BF16 in, F32 accumulate, M=128 N=64 K=16)
+//   warps 2-5 epilogue: tcgen05.ld 32x32b (thread t owns TMEM lane t = query
+//             row t), d = |a|^2 + |b|^2 - 2 a.b, per-row max-heap of K+16
+// Two TMEM accumulator stages let the MMA of tile i+1 overlap the epilogue of
+// tile i.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "knn.cuh"
+
+namespace grab {
+
+namespace tc {
+
+constexpr uint32_t BM = 128, BN = 64, KCH = 64;  // KCH: bf16 per 128-byte swizzle row
+constexpr uint32_t MAX_STAGES = 3;
+constexpr uint32_t KP_MAX = 80;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// K-major, 128-byte swizzle UMMA shared-memory descriptor (SM100 layout):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46)
+// = 1024 B between 8-row groups, version 1 at [46,48), layout 2 (SWIZZLE_128B) at [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: F32 accumulate, BF16 A/B, K-major, M=128, N=64
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t n, uint64_t key) {
+  uint32_t i = 0;
+  while (true) {
+    uint32_t l = 2 * i + 1, r = l + 1, big = i;
+    uint64_t kb = key;
+    if (l < n && h[l] > kb) {
+      big = l;
+      kb = h[l];
+    }
+    if (r < n && h[r] > kb) {
+      big = r;
+      kb = h[r];
+    }
+    if (big == i) break;
+    h[i] = h[big];
+    i = big;
+  }
+  h[i] = key;
+}
+
+struct Smem {
+  // all operand tiles are 1024-byte aligned (128B swizzle atom = 8 x 128 B)
+  static constexpr uint32_t kChunkA = BM * 128;  // one 64-bf16 K-chunk of the A tile
+  static constexpr uint32_t kChunkB = BN * 128;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_knn_screen_tc(const __grid_constant__ CUtensorMap tmap_ahi, const __grid_constant__ CUtensorMap tmap_alo,
+                    const __grid_constant__ CUtensorMap tmap_bhi, const __grid_constant__ CUtensorMap tmap_blo,
+                    const KnnJob* jobs, const Attr* attr, const float* norms, uint32_t nkc, uint32_t KP,
+                    uint32_t* cand, int causal, uint32_t STAGES) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t a_bytes = nkc * Smem::kChunkA;  // per hi / lo
+  const uint32_t b_bytes = nkc * Smem::kChunkB;
+  uint8_t* A_hi = smem;
+  uint8_t* A_lo = A_hi + a_bytes;
+  uint8_t* B = A_lo + a_bytes;  // STAGES x (hi, lo)
+  uint64_t* H = (uint64_t*)(B + STAGES * 2 * b_bytes);
+  uint64_t* bars = H + BM * KP;
+  uint64_t* a_full = bars;
+  uint64_t* b_full = bars + 1;
+  uint64_t* b_empty = b_full + MAX_STAGES;
+  uint64_t* acc_full = b_empty + MAX_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+
+  const KnnJob job = jobs[blockIdx.x];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ntiles = (job.c1 - job.c0 + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    mbar_init(a_full, 1);
+    for (uint32_t s = 0; s < STAGES; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (uint32_t i = threadIdx.x; i < BM * KP; i += blockDim.x) H[i] = ~0ull;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer
+      mbar_expect_tx(a_full, 2 * a_bytes);
+      for (uint32_t c = 0; c < nkc; ++c) {
+        tma_load_2d(A_hi + c * Smem::kChunkA, &tmap_ahi, a_full, (int32_t)(c * KCH), (int32_t)job.r0);
+        tma_load_2d(A_lo + c * Smem::kChunkA, &tmap_alo, a_full, (int32_t)(c * KCH), (int32_t)job.r0);
+      }
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t s = t % STAGES, round = t / STAGES;
+        mbar_wait(b_empty + s, (round & 1) ^ 1);
+        uint8_t* bh = B + s * 2 * b_bytes;
+        uint8_t* bl = bh + b_bytes;
+        mbar_expect_tx(b_full + s, 2 * b_bytes);
+        const int32_t row = (int32_t)(job.c0 + t * BN);
+        for (uint32_t c = 0; c < nkc; ++c) {
+          tma_load_2d(bh + c * Smem::kChunkB, &tmap_bhi, b_full + s, (int32_t)(c * KCH), row);
+          tma_load_2d(bl + c * Smem::kChunkB, &tmap_blo, b_full + s, (int32_t)(c * KCH), row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- UMMA issuer
+      mbar_wait(a_full, 0);
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t s = t % STAGES, round = t / STAGES;
+        const uint32_t as = t & 1, around = t >> 1;
+        mbar_wait(acc_empty + as, (around & 1) ^ 1);
+        mbar_wait(b_full + s, round & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d_tmem = tmem_base + as * BN;
+        const uint32_t bh = smem_u32(B + s * 2 * b_bytes), bl = bh + b_bytes;
+        const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo);
+        uint32_t acc = 0;
+        for (uint32_t c = 0; c < nkc; ++c) {
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {  // 4 x K=16 bf16 = 128 B per swizzle row
+            const uint32_t off = kk * 32;
+            const uint64_t dah = smem_desc(ah + c * Smem::kChunkA + off);
+            const uint64_t dal = smem_desc(al + c * Smem::kChunkA + off);
+            const uint64_t dbh = smem_desc(bh + c * Smem::kChunkB + off);
+            const uint64_t dbl = smem_desc(bl + c * Smem::kChunkB + off);
+            umma_bf16(d_tmem, dah, dbh, acc);
+            acc = 1;
+            umma_bf16(d_tmem, dah, dbl, 1);
+            umma_bf16(d_tmem, dal, dbh, 1);
+          }
+        }
+        umma_commit(b_empty + s);     // smem stage reusable once these MMAs retire
+        umma_commit(acc_full + as);   // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 = query rows
+    const uint32_t sub = warp & 3;
+    const uint32_t r = sub * 32 + lane;
+    const uint32_t prow = job.r0 + r;
+    const bool row_ok = r < job.nr && attr[prow].slot != kNoSlot;
+    const float a2 = row_ok ? norms[prow] : 0.f;
+    uint64_t* h = H + r * KP;
+    uint64_t top = ~0ull;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t as = t & 1, around = t >> 1;
+      mbar_wait(acc_full + as, around & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t taddr = tmem_base + ((sub * 32) << 16) + as * BN;
+      uint32_t v[4][16];
+      tmem_ld16(taddr + 0, v[0]);
+      tmem_ld16(taddr + 16, v[1]);
+      tmem_ld16(taddr + 32, v[2]);
+      tmem_ld16(taddr + 48, v[3]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + as);
+      if (row_ok) {
+        const uint32_t cb = job.c0 + t * BN;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+#pragma unroll
+          for (uint32_t j = 0; j < 16; ++j) {
+            const uint32_t c = cb + q * 16 + j;
+            if (c >= job.c1 || c == prow || (causal && c > prow)) continue;
+            const Attr ac = ld_attr(attr, c);
+            if (ac.slot == kNoSlot) continue;
+            const float d = fmaxf(a2 - 2.f * __uint_as_float(v[q][j]) + __ldg(norms + c), 0.f);
+            const uint64_t key = ((uint64_t)__float_as_uint(d) << 32) | c;
+            if (key < top) {
+              heap_replace_top(h, KP, key);
+              top = h[0];
+            }
+          }
+        }
+      }
+    }
+    if (row_ok)
+      for (uint32_t i = 0; i < KP; ++i) cand[(uint64_t)prow * KP + i] = h[i] == ~0ull ? kSentinel : (uint32_t)h[i];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+  }
+}
+
+// hi/lo BF16 split of the phys rows, K padded to a multiple of 64 (zeros)
+__global__ void k_split_bf16(const float* X, uint64_t rows, uint32_t dp, uint32_t kp, __nv_bfloat16* hi,
+                             __nv_bfloat16* lo) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * kp) return;
+  const uint64_t r = i / kp;
+  const uint32_t c = (uint32_t)(i % kp);
+  const float x = c < dp ? X[r * dp + c] : 0.f;
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  hi[i] = h;
+  lo[i] = __float2bfloat16_rn(x - __bfloat162float(h));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    GRAB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Error(GRAB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+static CUtensorMap make_map(void* base, uint64_t rows, uint32_t kp, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {kp, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
+  cuuint32_t box[2] = {KCH, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(GRAB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+}  // namespace tc
+
+bool knn_tc_supported(const DevIndex& ix, uint32_t KP) {
+  if (getenv("GRAB_KNN_SIMT")) return false;
+  const uint32_t kp = (ix.dp + tc::KCH - 1) / tc::KCH * tc::KCH;
+  return kp <= 128 && KP <= tc::KP_MAX;
+}
+
+void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, uint32_t njobs, uint32_t KP,
+                   uint32_t* cand, bool causal, cudaStream_t st) {
+  using namespace tc;
+  const uint32_t kp = (ix.dp + KCH - 1) / KCH * KCH;
+  const uint32_t nkc = kp / KCH;
+  const uint64_t rows = ix.phys_cap;
+  __nv_bfloat16 *hi, *lo;
+  GRAB_CUDA(cudaMallocAsync(&hi, rows * kp * 2, st));
+  GRAB_CUDA(cudaMallocAsync(&lo, rows * kp * 2, st));
+  k_split_bf16<<<(unsigned)div_up(rows * kp, 256), 256, 0, st>>>(ix.X, rows, ix.dp, kp, hi, lo);
+  GRAB_CHECK_LAUNCH();
+  const CUtensorMap ahi = make_map(hi, rows, kp, BM), alo = make_map(lo, rows, kp, BM);
+  const CUtensorMap bhi = make_map(hi, rows, kp, BN), blo = make_map(lo, rows, kp, BN);
+  uint32_t stages = MAX_STAGES;
+  size_t smem = 0;
+  for (; stages >= 2; --stages) {
+    smem = 1024 + 2 * (size_t)nkc * BM * 128 + stages * 2 * (size_t)nkc * BN * 128 + (size_t)BM * KP * 8 + 16 * 8;
+    if (smem <= 227 * 1024) break;
+  }
+  if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "tensor-core kNN tile exceeds shared memory");
+  GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_knn_screen_tc<<<njobs, 192, smem, st>>>(ahi, alo, bhi, blo, djobs, ix.attr, norms, nkc, KP, cand, causal ? 1 : 0,
+                                            stages);
+  GRAB_CHECK_LAUNCH();
+  GRAB_CUDA(cudaFreeAsync(hi, st));
+  GRAB_CUDA(cudaFreeAsync(lo, st));
+}
+
+}  // namespace grab
