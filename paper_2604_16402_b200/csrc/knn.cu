@@ -5,6 +5,9 @@
 // with the library's f64 distance tree and applies the exact (dist, tiebreak)
 // order, so the output equals the f64 oracle whenever the margin holds.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "knn.cuh"
 
@@ -13,25 +16,26 @@ namespace grab {
 constexpr uint32_t BM = kKnnBM, BN = 128, BK = 32;
 constexpr uint32_t kMargin = 16;
 
+// Max-heap (h[0] largest) of one row, element i at h[i * BM]: rows are
+// interleaved so neighbouring threads hit neighbouring banks.
 __device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t n, uint64_t key) {
-  // max-heap, h[0] is the largest; replace it with `key` and sift down
   uint32_t i = 0;
   while (true) {
     uint32_t l = 2 * i + 1, r = l + 1, big = i;
     uint64_t kb = key;
-    if (l < n && h[l] > kb) {
+    if (l < n && h[l * BM] > kb) {
       big = l;
-      kb = h[l];
+      kb = h[l * BM];
     }
-    if (r < n && h[r] > kb) {
+    if (r < n && h[r * BM] > kb) {
       big = r;
-      kb = h[r];
+      kb = h[r * BM];
     }
     if (big == i) break;
-    h[i] = h[big];
+    h[i * BM] = h[big * BM];
     i = big;
   }
-  h[i] = key;
+  h[i * BM] = key;
 }
 
 __global__ void __launch_bounds__(256) k_knn_screen(const KnnJob* jobs, const float* X, const Attr* attr,
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(256) k_knn_screen(const KnnJob* jobs, const fl
     __syncthreads();
     // epilogue 2: thread t < BM keeps row t's best KP by (screen dist, phys)
     if (my_row != kSentinel) {
-      uint64_t* h = H + t * KP;
+      uint64_t* h = H + t;
       uint64_t top = h[0];
       const uint32_t ncol = min(BN, job.c1 - cb);
       for (uint32_t j = 0; j < ncol; ++j) {
@@ -126,8 +130,9 @@ __global__ void __launch_bounds__(256) k_knn_screen(const KnnJob* jobs, const fl
     __syncthreads();
   }
   if (my_row != kSentinel && attr[my_row].slot != kNoSlot) {
-    uint64_t* h = H + t * KP;
-    for (uint32_t i = 0; i < KP; ++i) cand[(uint64_t)my_row * KP + i] = h[i] == ~0ull ? kSentinel : (uint32_t)h[i];
+    uint64_t* h = H + t;
+    for (uint32_t i = 0; i < KP; ++i)
+      cand[(uint64_t)my_row * KP + i] = h[i * BM] == ~0ull ? kSentinel : (uint32_t)h[i * BM];
   }
 }
 
@@ -211,7 +216,14 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
   KnnJob* dj;
   GRAB_CUDA(cudaMallocAsync(&dj, jobs.size() * sizeof(KnnJob), st));
   GRAB_CUDA(cudaMemcpyAsync(dj, jobs.data(), jobs.size() * sizeof(KnnJob), cudaMemcpyHostToDevice, st));
-  if (knn_tc_supported(ix, KP)) {
+  const bool dbg = getenv("GRAB_DEBUG") != nullptr;
+  auto clk = [&]() {
+    GRAB_CUDA(cudaStreamSynchronize(st));
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = dbg ? clk() : 0.0;
+  const bool use_tc = knn_tc_supported(ix, KP);
+  if (use_tc) {
     knn_screen_tc(ix, norms, dj, (uint32_t)jobs.size(), KP, cand, causal, st);
   } else {
     size_t smem = (size_t)BK * (BM + 4) * 4 + (size_t)BK * (BN + 4) * 4 + (size_t)BM * (BN + 1) * 4 +
@@ -221,6 +233,7 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
     k_knn_screen<<<(unsigned)jobs.size(), 256, smem, st>>>(dj, ix.X, ix.attr, norms, ix.dp, KP, cand, causal);
     GRAB_CHECK_LAUNCH();
   }
+  const double t1 = dbg ? clk() : 0.0;
   // rerank every row touched by a job
   std::vector<uint32_t> rows;
   for (const KnnJob& j : jobs)
@@ -250,6 +263,11 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
   else
     throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported");
   GRAB_CUDA(cudaStreamSynchronize(st));
+  if (dbg) {
+    const double t2 = clk();
+    fprintf(stderr, "[grab] knn jobs=%zu K=%u %s screen %.3f s, rerank %.3f s\n", jobs.size(), K,
+            use_tc ? "tcgen05" : "simt", t1 - t0, t2 - t1);
+  }
   cudaFreeAsync(dr, st);
   cudaFreeAsync(dj, st);
   cudaFreeAsync(cand, st);

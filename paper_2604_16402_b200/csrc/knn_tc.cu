@@ -106,24 +106,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
+// Max-heap of n keys for one row, element i at h[i * BM] (rows interleaved so
+// the 32 lanes of a warp touch 32 consecutive words: no bank conflicts).
 __device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t n, uint64_t key) {
   uint32_t i = 0;
   while (true) {
     uint32_t l = 2 * i + 1, r = l + 1, big = i;
     uint64_t kb = key;
-    if (l < n && h[l] > kb) {
+    if (l < n && h[l * BM] > kb) {
       big = l;
-      kb = h[l];
+      kb = h[l * BM];
     }
-    if (r < n && h[r] > kb) {
+    if (r < n && h[r * BM] > kb) {
       big = r;
-      kb = h[r];
+      kb = h[r * BM];
     }
     if (big == i) break;
-    h[i] = h[big];
+    h[i * BM] = h[big * BM];
     i = big;
   }
-  h[i] = key;
+  h[i * BM] = key;
 }
 
 struct Smem {
@@ -132,11 +134,13 @@ struct Smem {
   static constexpr uint32_t kChunkB = BN * 128;
 };
 
-__global__ void __launch_bounds__(192, 1)
+constexpr uint32_t kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
+
+__global__ void __launch_bounds__(kThreads, 1)
     k_knn_screen_tc(const __grid_constant__ CUtensorMap tmap_ahi, const __grid_constant__ CUtensorMap tmap_alo,
                     const __grid_constant__ CUtensorMap tmap_bhi, const __grid_constant__ CUtensorMap tmap_blo,
-                    const KnnJob* jobs, const Attr* attr, const float* norms, uint32_t nkc, uint32_t KP,
-                    uint32_t* cand, int causal, uint32_t STAGES) {
+                    const KnnJob* jobs, const Attr* attr, const float* row_norms, const float* norms,
+                    uint32_t nkc, uint32_t KP, uint32_t* cand, int causal, uint32_t STAGES, uint32_t NG) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t a_bytes = nkc * Smem::kChunkA;  // per hi / lo
@@ -144,8 +148,8 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* A_hi = smem;
   uint8_t* A_lo = A_hi + a_bytes;
   uint8_t* B = A_lo + a_bytes;  // STAGES x (hi, lo)
-  uint64_t* H = (uint64_t*)(B + STAGES * 2 * b_bytes);
-  uint64_t* bars = H + BM * KP;
+  uint64_t* H = (uint64_t*)(B + STAGES * 2 * b_bytes);  // NG column groups x [KP][BM]
+  uint64_t* bars = H + NG * BM * KP;
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
   uint64_t* b_empty = b_full + MAX_STAGES;
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, 4);
+      mbar_init(acc_empty + s, 4 * NG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(192, 1)
                  "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (uint32_t i = threadIdx.x; i < BM * KP; i += blockDim.x) H[i] = ~0ull;
+  for (uint32_t i = threadIdx.x; i < NG * BM * KP; i += blockDim.x) H[i] = ~0ull;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -235,50 +239,90 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ---- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 = query rows
-    const uint32_t sub = warp & 3;
+    // ---- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 = query rows;
+    // with NG = 2 two warps share a sub-partition, each owning half of every
+    // tile's columns and a private heap per row (merged at the end).
+    const uint32_t e = warp - 2, sub = warp & 3, grp = e >> 2;
     const uint32_t r = sub * 32 + lane;
     const uint32_t prow = job.r0 + r;
-    const bool row_ok = r < job.nr && attr[prow].slot != kNoSlot;
-    const float a2 = row_ok ? norms[prow] : 0.f;
-    uint64_t* h = H + r * KP;
+    const bool active = grp < NG;
+    const bool row_ok = active && r < job.nr && attr[prow].slot != kNoSlot;
+    const float a2 = row_ok ? row_norms[prow] : 0.f;
+    uint64_t* h = H + grp * BM * KP + r;  // interleaved: element i at h[i * BM]
     uint64_t top = ~0ull;
-    for (uint32_t t = 0; t < ntiles; ++t) {
+    const uint32_t QN = 4 / NG;  // 16-column chunks per warp per tile
+    for (uint32_t t = 0; active && t < ntiles; ++t) {
       const uint32_t as = t & 1, around = t >> 1;
       mbar_wait(acc_full + as, around & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t taddr = tmem_base + ((sub * 32) << 16) + as * BN;
+      const uint32_t col0 = grp * QN * 16;
+      const uint32_t taddr = tmem_base + ((sub * 32) << 16) + as * BN + col0;
       uint32_t v[4][16];
       tmem_ld16(taddr + 0, v[0]);
       tmem_ld16(taddr + 16, v[1]);
-      tmem_ld16(taddr + 32, v[2]);
-      tmem_ld16(taddr + 48, v[3]);
+      if (QN == 4) {
+        tmem_ld16(taddr + 32, v[2]);
+        tmem_ld16(taddr + 48, v[3]);
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + as);
       if (row_ok) {
-        const uint32_t cb = job.c0 + t * BN;
+        const uint32_t cb = job.c0 + t * BN + col0;
+        // |b|^2 with +inf for headroom rows / past the tile's end (one broadcast
+        // float4 load per 4 columns); the heap key is only built for survivors
+        // of an f32 threshold test against the current K'-th distance.
+        const float thr = top == ~0ull ? INFINITY : __uint_as_float((uint32_t)(top >> 32));
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
+          if (q >= QN) break;
+          // branch-free pass over 16 columns: distances + survivor mask
+          float d[16];
+          uint32_t hit = 0;
 #pragma unroll
-          for (uint32_t j = 0; j < 16; ++j) {
-            const uint32_t c = cb + q * 16 + j;
-            if (c >= job.c1 || c == prow || (causal && c > prow)) continue;
-            const Attr ac = ld_attr(attr, c);
-            if (ac.slot == kNoSlot) continue;
-            const float d = fmaxf(a2 - 2.f * __uint_as_float(v[q][j]) + __ldg(norms + c), 0.f);
-            const uint64_t key = ((uint64_t)__float_as_uint(d) << 32) | c;
-            if (key < top) {
-              heap_replace_top(h, KP, key);
-              top = h[0];
+          for (uint32_t j4 = 0; j4 < 4; ++j4) {
+            const float4 n4 = __ldg(reinterpret_cast<const float4*>(norms + cb + q * 16) + j4);
+            const float b2[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+              const uint32_t j = 4 * j4 + u;
+              d[j] = fmaxf(fmaf(-2.f, __uint_as_float(v[q][j]), a2 + b2[u]), 0.f);
+              hit |= (uint32_t)(d[j] <= thr) << j;
+            }
+          }
+          if (hit) {  // rare after the first tiles: columns at or below the K'-th distance
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+              const uint32_t c = cb + q * 16 + j;
+              if (((hit >> j) & 1u) && d[j] < INFINITY && c != prow && c < job.c1 && !(causal && c > prow)) {
+                const uint64_t key = ((uint64_t)__float_as_uint(d[j]) << 32) | c;
+                if (key < top) {
+                  heap_replace_top(h, KP, key);
+                  top = h[0];
+                }
+              }
             }
           }
         }
       }
     }
-    if (row_ok)
-      for (uint32_t i = 0; i < KP; ++i) cand[(uint64_t)prow * KP + i] = h[i] == ~0ull ? kSentinel : (uint32_t)h[i];
+    // merge the column groups' heaps (group 0 absorbs group 1), then emit
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads - 64));
+    if (row_ok && grp == 0) {
+      for (uint32_t g = 1; g < NG; ++g) {
+        const uint64_t* o = H + g * BM * KP + r;
+        for (uint32_t i = 0; i < KP; ++i) {
+          const uint64_t key = o[i * BM];
+          if (key < top) {
+            heap_replace_top(h, KP, key);
+            top = h[0];
+          }
+        }
+      }
+      for (uint32_t i = 0; i < KP; ++i)
+        cand[(uint64_t)prow * KP + i] = h[i * BM] == ~0ull ? kSentinel : (uint32_t)h[i * BM];
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -286,6 +330,11 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
   }
+}
+
+__global__ void k_mask_norms(const float* norms, const Attr* attr, uint64_t rows, uint64_t padded, float* out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < padded) out[i] = (i < rows && attr[i].slot != kNoSlot) ? norms[i] : INFINITY;
 }
 
 // hi/lo BF16 split of the phys rows, K padded to a multiple of 64 (zeros)
@@ -349,19 +398,35 @@ void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, 
   GRAB_CUDA(cudaMallocAsync(&lo, rows * kp * 2, st));
   k_split_bf16<<<(unsigned)div_up(rows * kp, 256), 256, 0, st>>>(ix.X, rows, ix.dp, kp, hi, lo);
   GRAB_CHECK_LAUNCH();
+  // candidate |b|^2, +inf for headroom rows and the padding after the last tile
+  const uint64_t padded = div_up(rows, BN) * BN + BN;
+  float* nm;
+  GRAB_CUDA(cudaMallocAsync(&nm, padded * 4, st));
+  k_mask_norms<<<(unsigned)div_up(padded, 256), 256, 0, st>>>(norms, ix.attr, rows, padded, nm);
+  GRAB_CHECK_LAUNCH();
   const CUtensorMap ahi = make_map(hi, rows, kp, BM), alo = make_map(lo, rows, kp, BM);
   const CUtensorMap bhi = make_map(hi, rows, kp, BN), blo = make_map(lo, rows, kp, BN);
-  uint32_t stages = MAX_STAGES;
+  // prefer two epilogue column groups (8 epilogue warps), then the deepest B ring that fits
+  uint32_t stages = 0, ng = 0;
   size_t smem = 0;
-  for (; stages >= 2; --stages) {
-    smem = 1024 + 2 * (size_t)nkc * BM * 128 + stages * 2 * (size_t)nkc * BN * 128 + (size_t)BM * KP * 8 + 16 * 8;
-    if (smem <= 227 * 1024) break;
+  for (uint32_t g = 2; g >= 1 && !stages; --g) {
+    for (uint32_t s = MAX_STAGES; s >= 2; --s) {
+      const size_t b = 1024 + 2 * (size_t)nkc * BM * 128 + s * 2 * (size_t)nkc * BN * 128 +
+                       (size_t)g * BM * KP * 8 + 16 * 8;
+      if (b <= 227 * 1024) {
+        stages = s;
+        ng = g;
+        smem = b;
+        break;
+      }
+    }
   }
-  if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "tensor-core kNN tile exceeds shared memory");
+  if (!stages) throw Error(GRAB_ERR_VALUE, "tensor-core kNN tile exceeds shared memory");
   GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_knn_screen_tc<<<njobs, 192, smem, st>>>(ahi, alo, bhi, blo, djobs, ix.attr, norms, nkc, KP, cand, causal ? 1 : 0,
-                                            stages);
+  k_knn_screen_tc<<<njobs, kThreads, smem, st>>>(ahi, alo, bhi, blo, djobs, ix.attr, norms, nm, nkc, KP, cand,
+                                                 causal ? 1 : 0, stages, ng);
   GRAB_CHECK_LAUNCH();
+  GRAB_CUDA(cudaFreeAsync(nm, st));
   GRAB_CUDA(cudaFreeAsync(hi, st));
   GRAB_CUDA(cudaFreeAsync(lo, st));
 }
