@@ -294,8 +294,10 @@ def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None =
         raise ValueError(f"unknown bucket strategy: {bucket_strategy!r}")
     dev = _is_dev(vectors)
     if dev:
+        import torch
         V = vectors.contiguous()
         S = scalars.contiguous()
+        torch.cuda.current_stream(V.device).synchronize()  # the library works on its own stream
         n, dim = V.shape
         mem = L.MEM_DEVICE
     else:
@@ -366,8 +368,10 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
     """Integrate one batch on the device: append, candidates, forward pruning, reverse rewiring, healing."""
     dev = _is_dev(vectors)
     if dev:
+        import torch
         V = vectors.contiguous()
         S = scalars.contiguous()
+        torch.cuda.current_stream(V.device).synchronize()  # the library works on its own stream
         b = V.shape[0]
         mem = L.MEM_DEVICE
         Ih = None if ids is None else np.ascontiguousarray(ids.cpu().numpy() if hasattr(ids, "cpu") else ids,

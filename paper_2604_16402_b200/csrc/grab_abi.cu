@@ -203,7 +203,7 @@ extern "C" int grab_search(const grab_index* h, const float* queries, uint64_t n
     if (p->itopk > 2048) throw Error(GRAB_ERR_VALUE, "itopk > 2048 not supported");
     if (nq == 0) return;
     if (nq >= 0xFFFFFFFFull) throw Error(GRAB_ERR_VALUE, "too many queries in one batch");
-    cudaStream_t st = mem == GRAB_MEM_DEVICE && stream ? (cudaStream_t)stream : ix.stream;
+    cudaStream_t st = mem == GRAB_MEM_DEVICE ? (cudaStream_t)stream : ix.stream;  // device mode: the caller's stream (NULL = legacy default)
     uint64_t nr = range_stride ? nq : 1;
     if (mem == GRAB_MEM_HOST) {
       for (uint64_t i = 0; i < nr; ++i)
@@ -259,7 +259,7 @@ extern "C" int grab_brute_force(const grab_index* h, const float* queries, uint6
     set_device(ix);
     if (k < 1) throw Error(GRAB_ERR_VALUE, "k must be >= 1");
     if (nq == 0) return;
-    cudaStream_t st = mem == GRAB_MEM_DEVICE && stream ? (cudaStream_t)stream : ix.stream;
+    cudaStream_t st = mem == GRAB_MEM_DEVICE ? (cudaStream_t)stream : ix.stream;  // device mode: the caller's stream (NULL = legacy default)
     uint64_t nr = range_stride ? nq : 1;
     DBuf bq, blo, bhi, bs, bd, bc;
     const float* Q = padded_rows(ix, queries, nq, mem, bq, st);
@@ -288,7 +288,7 @@ extern "C" int grab_bucket_select(const grab_index* h, const double* lower, cons
     set_device(ix);
     if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no bucket metadata (never built)");
     if (!n) return;
-    cudaStream_t st = mem == GRAB_MEM_DEVICE && stream ? (cudaStream_t)stream : ix.stream;
+    cudaStream_t st = mem == GRAB_MEM_DEVICE ? (cudaStream_t)stream : ix.stream;  // device mode: the caller's stream (NULL = legacy default)
     DBuf a, b, c, d;
     const double* lo = stage_in(lower, n, mem, a, st);
     const double* hi = stage_in(upper, n, mem, b, st);
@@ -309,7 +309,7 @@ extern "C" int grab_bucket_ids(const grab_index* h, const float* scalars, uint64
     set_device(ix);
     if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no bucket metadata (never built)");
     if (!n) return;
-    cudaStream_t st = mem == GRAB_MEM_DEVICE && stream ? (cudaStream_t)stream : ix.stream;
+    cudaStream_t st = mem == GRAB_MEM_DEVICE ? (cudaStream_t)stream : ix.stream;  // device mode: the caller's stream (NULL = legacy default)
     DBuf a, c;
     const float* s = stage_in(scalars, n, mem, a, st);
     int32_t* o = stage_out(out, n, mem, c, st);
@@ -360,6 +360,7 @@ extern "C" int grab_import(grab_index* h, uint64_t n, const float* X, const floa
     for (uint64_t i = 0; i < n; ++i) ix.ids[i] = (int64_t)i;
     ix.count = n;
     ix.built = true;
+    ix.adj_version++;
     GRAB_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -431,7 +432,9 @@ extern "C" int grab_build(grab_index* h, const float* vectors, const float* scal
     std::lock_guard<std::mutex> lk(h->writer);
     DevIndex& ix = h->ix;
     set_device(ix);
+    ix.adj_version++;
     build_index_device(ix, vectors, scalars, n, strategy, k_g, refine_rounds, mem, report);
+    ix.adj_version++;
   });
 }
 
@@ -443,7 +446,9 @@ extern "C" int grab_build_ex(grab_index* h, const float* vectors, const float* s
     std::lock_guard<std::mutex> lk(h->writer);
     DevIndex& ix = h->ix;
     set_device(ix);
+    ix.adj_version++;
     build_index_device(ix, vectors, scalars, n, strategy, k_g, refine_rounds, mem, report, debug);
+    ix.adj_version++;
   });
 }
 
@@ -454,7 +459,9 @@ extern "C" int grab_insert(grab_index* h, const float* vectors, const float* sca
     std::lock_guard<std::mutex> lk(h->writer);
     DevIndex& ix = h->ix;
     set_device(ix);
+    ix.adj_version++;
     insert_batch_device(ix, vectors, scalars, ids, b, search_itopk, mem, report);
+    ix.adj_version++;
   });
 }
 

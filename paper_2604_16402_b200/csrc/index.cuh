@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -43,6 +45,14 @@ struct DevIndex {
   float* X = nullptr;     // [phys_cap x dp]
   Attr* attr = nullptr;   // [phys_cap]
   uint32_t* adj = nullptr;  // [phys_cap x k_max], phys ids
+  // Search-side mirror of the adjacency: adja[p*K + j] = attr[adj[p*K + j]]
+  // ({NaN, kNoSlot} for SENTINEL), so one coalesced row load gives every
+  // neighbour's pre-check scalar and slot without a random 8-byte gather per
+  // neighbour. Rebuilt lazily by the search path when adj_version moved.
+  uint64_t adj_version = 1;  // bumped by every adjacency / layout mutation
+  mutable Attr* adja = nullptr;
+  mutable uint64_t adja_rows = 0, adja_version = 0;
+  std::shared_ptr<std::mutex> adja_mu = std::make_shared<std::mutex>();
 
   // buckets
   uint32_t m = 0;
@@ -62,6 +72,8 @@ struct DevIndex {
 // ---- layout.cu ----
 void index_alloc_slots(DevIndex& ix);
 void index_free(DevIndex& ix);
+// (re)build ix.adja if the adjacency changed since the last search (search.cu)
+void ensure_adja(const DevIndex& ix, cudaStream_t st);
 // Lay out `count` slots whose bucket ids are in ix.i2b (device) and whose
 // vectors/scalars are given in slot order (device pointers, rows of `dim`).
 // Members of a bucket are ordered by ascending slot. Allocates slabs with

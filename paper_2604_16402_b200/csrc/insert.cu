@@ -616,6 +616,7 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
     a.out_dists = found_d;
     a.out_counts = found_cnt;
     a.out_stats = nullptr;
+    ix.adj_version++;  // append / relayout changed rows since the last search
     run_search(ix, a, st);
   }
   mark(2);

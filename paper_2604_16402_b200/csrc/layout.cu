@@ -33,6 +33,10 @@ static void free_phys(DevIndex& ix) {
   cfree(ix.X);
   cfree(ix.attr);
   cfree(ix.adj);
+  cfree(ix.adja);
+  ix.adja = nullptr;
+  ix.adja_rows = 0;
+  ix.adj_version++;
   ix.X = nullptr;
   ix.attr = nullptr;
   ix.adj = nullptr;
@@ -257,6 +261,7 @@ static void relayout(DevIndex& ix, const std::vector<uint32_t>& extra) {
   ix.X = nullptr;
   ix.attr = nullptr;
   ix.adj = nullptr;
+  ix.adj_version++;
   alloc_phys(ix, total);
   uint32_t *d_os, *d_ns, *d_oc, *d_pb, *d_remap;
   GRAB_CUDA(cudaMalloc(&d_os, m * 4));

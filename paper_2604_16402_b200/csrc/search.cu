@@ -52,31 +52,42 @@ void upload_pcg_jump_tables() {
 __device__ __forceinline__ uint32_t hash32(uint32_t k) { return k * 0x9E3779B1u; }
 
 // Open-addressing set of 2^lg u32 entries (value key+1, 0 = empty).
-// Probe loops are written with a single structured exit: early returns from
-// inside a data-dependent loop make the warp look unconverged to the compiler
-// and turn every later shuffle into the slow collective fallback.
-__device__ __forceinline__ bool set_insert(uint32_t* tab, uint32_t lg, uint32_t key) {
+// Every probe loop is warp-uniform (all 32 lanes iterate until no lane has a
+// pending probe): a per-lane trip count would leave the warp diverged, and a
+// diverged warp runs every later shuffle/ballot through the slow collective
+// path (BRA.DIV) -- measured at ~95% of all warp ops before this rule.
+// Returns true for active lanes whose key was absent (and is now inserted).
+__device__ __forceinline__ bool set_insert_w(uint32_t* tab, uint32_t lg, uint32_t key, bool active) {
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
   const uint32_t v = key + 1;
-  uint32_t cur = atomicCAS(tab + h, 0u, v);
-  while (cur != 0u && cur != v) {
-    h = (h + 1) & mask;
-    cur = atomicCAS(tab + h, 0u, v);
+  uint32_t cur = active ? atomicCAS(tab + h, 0u, v) : 0u;
+  bool pending = active && cur != 0u && cur != v;
+  while (__any_sync(0xFFFFFFFFu, pending)) {
+    if (pending) {
+      h = (h + 1) & mask;
+      cur = atomicCAS(tab + h, 0u, v);
+      pending = cur != 0u && cur != v;
+    }
   }
-  return cur == 0u;
+  return active && cur == 0u;
 }
 
-__device__ __forceinline__ bool set_contains(const uint32_t* tab, uint32_t lg, uint32_t key) {
+// True for active lanes whose key is present.
+__device__ __forceinline__ bool set_contains_w(const uint32_t* tab, uint32_t lg, uint32_t key, bool active) {
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
   const uint32_t v = key + 1;
-  uint32_t cur = *((volatile const uint32_t*)(tab + h));
-  while (cur != 0u && cur != v) {
-    h = (h + 1) & mask;
-    cur = *((volatile const uint32_t*)(tab + h));
+  uint32_t cur = active ? *((volatile const uint32_t*)(tab + h)) : 0u;
+  bool pending = active && cur != 0u && cur != v;
+  while (__any_sync(0xFFFFFFFFu, pending)) {
+    if (pending) {
+      h = (h + 1) & mask;
+      cur = *((volatile const uint32_t*)(tab + h));
+      pending = cur != 0u && cur != v;
+    }
   }
-  return cur == v;
+  return active && cur == v;
 }
 
 __device__ __forceinline__ void clear_words(uint32_t* p, uint32_t n) {
@@ -88,33 +99,40 @@ __device__ __forceinline__ void clear_words(uint32_t* p, uint32_t n) {
 // ---------------------------------------------------------------- layout
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
+// Per-warp shared memory. The queue is an array of 16-byte entries
+// {f64 distance, slot, phys | kExpanded} kept sorted by (distance, slot), so a
+// merge moves one LDS.128/STS.128 per displaced entry.
 struct WarpLayout {
-  uint32_t qd, qs, qp, qf, cd, cs, cp, dd, fr, bytes;
+  uint32_t qe, cd, cs, cp, rr, dd, fr, bytes;
 };
 
 __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
   WarpLayout l;
   uint32_t o = 0;
-  l.qd = o;
-  o += align16(s.itopk * 8);
+  l.qe = o;
+  o += s.itopk * 16;
   l.cd = o;
   o += align16(s.cmax * 8);
-  l.qs = o;
-  o += align16(s.itopk * 4);
-  l.qp = o;
-  o += align16(s.itopk * 4);
   l.cs = o;
   o += align16(s.cmax * 4);
   l.cp = o;
+  o += align16(s.cmax * 4);
+  l.rr = o;
   o += align16(s.cmax * 4);
   l.dd = o;
   o += align16(s.dsz * 4);
   l.fr = o;
   o += align16(s.width * 4);
-  l.qf = o;
-  o += align16(s.itopk);
   l.bytes = o;
   return l;
+}
+
+constexpr uint32_t kExpanded = 0x80000000u;  // queue entry flag (phys ids < 2^31)
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ double qe_dist(const uint4& e) { return __hiloint2double((int)e.y, (int)e.x); }
+__device__ __forceinline__ uint4 qe_pack(double d, uint32_t s, uint32_t p) {
+  return make_uint4((uint32_t)__double2loint(d), (uint32_t)__double2hiint(d), s, p);
 }
 
 // ---------------------------------------------------------------- distances
@@ -137,12 +155,14 @@ struct GroupOf {
   static constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : (NC <= 4 ? 2 : 1));
 };
 
-// Distances for cand[0..n): writes cd[i]. All lanes participate.
+// Distances for cand[0..n): writes cd[i]. All lanes participate; G rows are in
+// flight per round (16-byte ld.global.nc per lane per 128-float chunk).
 template <int NC>
 __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __restrict__ X, uint32_t dp,
                                       const uint32_t* cp, double* cd, uint32_t n) {
   constexpr int G = GroupOf<NC>::G;
   const uint32_t lane = lane_id();
+  __syncwarp();
   for (uint32_t base = 0; base < n; base += G) {
     float4 x[G][NC];
 #pragma unroll
@@ -164,6 +184,7 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
       for (int c = 0; c < NC; ++c) acc = sq4(x[g][c], qr.q[c], acc);
       part[g] = acc;
     }
+    __syncwarp();
     const double v = reduce_scatter<G>(part);
     constexpr uint32_t SPAN = 32 / G;  // lanes holding each candidate's sum
     const uint32_t g = lane / SPAN;
@@ -173,12 +194,14 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
 }
 
 // ---------------------------------------------------------------- queue ops
+// Shared-memory bitonic sort of (d, s, p)[0..n) padded to P (power of 2); used
+// only when more than 32 candidates survive (queue filling up).
 __device__ __forceinline__ void bitonic_sort(double* d, uint32_t* s, uint32_t* p, uint32_t n, uint32_t P) {
   const uint32_t lane = lane_id();
   for (uint32_t i = n + lane; i < P; i += 32) {
     d[i] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-    s[i] = 0xFFFFFFFFu;
-    p[i] = 0xFFFFFFFFu;
+    s[i] = kFull;
+    p[i] = kFull;
   }
   __syncwarp();
   for (uint32_t k = 2; k <= P; k <<= 1) {
@@ -205,27 +228,66 @@ __device__ __forceinline__ void bitonic_sort(double* d, uint32_t* s, uint32_t* p
   }
 }
 
-// number of entries in sorted (d,s)[0..n) strictly less than key
-__device__ __forceinline__ uint32_t rank_in(const double* d, const uint32_t* s, uint32_t n, double kd, uint32_t ks) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (key_less(d[mid], s[mid], kd, ks))
-      lo = mid + 1;
-    else
-      hi = mid;
+// Register bitonic sort of one (d, s, p) per lane, ascending across lanes.
+__device__ __forceinline__ void warp_sort32(double& d, uint32_t& s, uint32_t& p) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const double od = __shfl_xor_sync(kFull, d, j);
+      const uint32_t os = __shfl_xor_sync(kFull, s, j);
+      const uint32_t op = __shfl_xor_sync(kFull, p, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      const bool olt = key_less(od, os, d, s);
+      if ((lower == up) ? olt : !olt) {
+        d = od;
+        s = os;
+        p = op;
+      }
+    }
   }
-  return lo;
 }
 
-// CandidateQueue.admit: merge cand[0..nc) into the queue (length L) in place,
-// truncated to itopk. Returns the new length.
-__device__ __forceinline__ uint32_t admit(double* qd, uint32_t* qs, uint32_t* qp, uint8_t* qf, double* cd,
-                                          uint32_t* cs, uint32_t* cp, uint32_t L, uint32_t nc, uint32_t itopk) {
+// Number of queue entries strictly less than (kd, ks): branch-free lower bound
+// with a warp-uniform step count (no divergence).
+__device__ __forceinline__ uint32_t rank_in_queue(const uint4* qe, uint32_t L, double kd, uint32_t ks) {
+  uint32_t pos = 0;
+  for (uint32_t step = L ? (1u << (31 - __clz(L))) : 0u; step > 0; step >>= 1) {
+    const uint32_t probe = pos + step;
+    if (probe <= L) {
+      const double* qd = reinterpret_cast<const double*>(qe + probe - 1);
+      const uint32_t qs = reinterpret_cast<const uint32_t*>(qe + probe - 1)[2];
+      if (key_less(*qd, qs, kd, ks)) pos = probe;
+    }
+  }
+  return pos;
+}
+
+// #{j < n : rr[j] <= i} over the nondecreasing rank array rr.
+__device__ __forceinline__ uint32_t upper_rank(const uint32_t* rr, uint32_t n, uint32_t i) {
+  uint32_t pos = 0;
+  for (uint32_t step = 1u << (31 - __clz(n)); step > 0; step >>= 1) {
+    const uint32_t probe = pos + step;
+    if (probe <= n && rr[probe - 1] <= i) pos = probe;
+  }
+  return pos;
+}
+
+// CandidateQueue.admit (searcher.py:64-71): merge the nc candidates (cd, cs,
+// cp) into the queue of length L in place, truncated to itopk. Candidates that
+// cannot survive truncation are dropped first; the survivors are sorted (in
+// registers when <= 32), ranked against the queue by binary search, and every
+// displaced queue entry moves once. `fu` (first-unexpanded hint) is lowered to
+// the first new entry. Returns the new length.
+__device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, uint32_t* cp, uint32_t* rr, uint32_t L,
+                                          uint32_t nc, uint32_t itopk, uint32_t& fu) {
   const uint32_t lane = lane_id();
-  if (L == itopk && nc) {  // candidates that cannot survive truncation are dropped up front
-    const double td = qd[L - 1];
-    const uint32_t ts = qs[L - 1];
+  if (L == itopk && nc) {
+    const uint4 te = qe[L - 1];
+    const double td = qe_dist(te);
+    const uint32_t ts = te.z;
     uint32_t kept = 0;
     for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
       const uint32_t i = b0 + lane;
@@ -238,7 +300,7 @@ __device__ __forceinline__ uint32_t admit(double* qd, uint32_t* qs, uint32_t* qp
         p = cp[i];
         ok = key_less(d, s, td, ts);
       }
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+      const uint32_t m = __ballot_sync(kFull, ok);
       __syncwarp();
       if (ok) {
         const uint32_t pos = kept + __popc(m & ((1u << lane) - 1));
@@ -252,47 +314,63 @@ __device__ __forceinline__ uint32_t admit(double* qd, uint32_t* qs, uint32_t* qp
     nc = kept;
   }
   if (nc == 0) return L;
-  uint32_t P = 32;
-  while (P < nc) P <<= 1;
-  bitonic_sort(cd, cs, cp, nc, P);
-  // candidate destinations against the OLD queue (<= 4 per lane, cmax <= 128 on this path)
-  uint32_t cpos[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const uint32_t j = lane + 32 * t;
-    cpos[t] = j < nc ? j + rank_in(qd, qs, L, cd[j], cs[j]) : 0xFFFFFFFFu;
-  }
-  // move queue entries, highest chunk first (destinations are >= sources)
-  for (int32_t b0 = (int32_t)((L - 1) & ~31u); b0 >= 0; b0 -= 32) {
-    const uint32_t i = (uint32_t)b0 + lane;
-    double d = 0;
-    uint32_t s = 0, p = 0, pos = 0xFFFFFFFFu;
-    uint8_t f = 0;
-    if (i < L) {
-      d = qd[i];
-      s = qs[i];
-      p = qp[i];
-      f = qf[i];
-      pos = i + rank_in(cd, cs, nc, d, s);
+  const double kInf = __longlong_as_double(0x7FF0000000000000ll);
+  if (nc <= 32) {
+    double d = kInf;
+    uint32_t s = kFull, p = kFull;
+    if (lane < nc) {
+      d = cd[lane];
+      s = cs[lane];
+      p = cp[lane];
     }
+    warp_sort32(d, s, p);
+    const uint32_t r = rank_in_queue(qe, L, d, s);
+    rr[lane] = r;
     __syncwarp();
-    if (pos < itopk) {
-      qd[pos] = d;
-      qs[pos] = s;
-      qp[pos] = p;
-      qf[pos] = f;
+    const uint32_t r0 = __shfl_sync(kFull, r, 0);
+    if (r0 < L) {
+      for (int32_t b0 = (int32_t)((L - 1) & ~31u); b0 >= (int32_t)(r0 & ~31u); b0 -= 32) {
+        const uint32_t i = (uint32_t)b0 + lane;
+        uint4 e;
+        uint32_t dst = kFull;
+        if (i < L && i >= r0) {
+          e = qe[i];
+          dst = i + upper_rank(rr, nc, i);
+        }
+        __syncwarp();
+        if (dst < itopk) qe[dst] = e;
+        __syncwarp();
+      }
     }
+    const uint32_t pos = lane + r;
+    if (lane < nc && pos < itopk) qe[pos] = qe_pack(d, s, p);
+    fu = min(fu, r0);
+  } else {
+    uint32_t P = 64;
+    while (P < nc) P <<= 1;
+    bitonic_sort(cd, cs, cp, nc, P);
+    for (uint32_t j = lane; j < nc; j += 32) rr[j] = rank_in_queue(qe, L, cd[j], cs[j]);
     __syncwarp();
-  }
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const uint32_t j = lane + 32 * t;
-    if (cpos[t] < itopk) {
-      qd[cpos[t]] = cd[j];
-      qs[cpos[t]] = cs[j];
-      qp[cpos[t]] = cp[j];
-      qf[cpos[t]] = 0;
+    const uint32_t r0 = rr[0];
+    if (r0 < L) {
+      for (int32_t b0 = (int32_t)((L - 1) & ~31u); b0 >= (int32_t)(r0 & ~31u); b0 -= 32) {
+        const uint32_t i = (uint32_t)b0 + lane;
+        uint4 e;
+        uint32_t dst = kFull;
+        if (i < L && i >= r0) {
+          e = qe[i];
+          dst = i + upper_rank(rr, nc, i);
+        }
+        __syncwarp();
+        if (dst < itopk) qe[dst] = e;
+        __syncwarp();
+      }
     }
+    for (uint32_t j = lane; j < nc; j += 32) {
+      const uint32_t pos = j + rr[j];
+      if (pos < itopk) qe[pos] = qe_pack(cd[j], cs[j], cp[j]);
+    }
+    fu = min(fu, r0);
   }
   __syncwarp();
   return min(itopk, L + nc);
@@ -313,6 +391,7 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
   const uint64_t total = a.bcum[hi_b + 1] - c0;
   uint32_t picked = 0;
   *attempts = 0;
+  const uint32_t bstep = hi_b > lo_b ? 1u << (31 - __clz(hi_b - lo_b)) : 0u;
   if (total > 0) {
     const uint32_t ndraw = 4 * want;
     *attempts = ndraw;
@@ -347,14 +426,9 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
         float sv = 0.f;
         if (have) {
           const uint64_t f = c0 + stage[off + lane];
-          uint32_t lo = lo_b, hi = hi_b;  // bucket b with bcum[b] <= f < bcum[b+1]
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (__ldg(a.bcum + mid) <= f)
-              lo = mid;
-            else
-              hi = mid - 1;
-          }
+          uint32_t lo = lo_b;  // last bucket b in [lo_b, hi_b] with bcum[b] <= f (warp-uniform steps)
+          for (uint32_t step = bstep; step > 0; step >>= 1)
+            if (lo + step <= hi_b && __ldg(a.bcum + lo + step) <= f) lo += step;
           phys = __ldg(a.bstart + lo) + (uint32_t)(f - __ldg(a.bcum + lo));
           const Attr at = ld_attr(a.attr, phys);
           slot = at.slot;
@@ -363,12 +437,13 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
         const bool inr = have && slot < a.n_live && sv >= lo_f && sv <= hi_f;
         const uint32_t same = __match_any_sync(0xFFFFFFFFu, inr ? phys : 0xFFFFFFFFu);
         const bool first = inr && (uint32_t)(__ffs(same) - 1) == lane;
-        const bool fresh = first && !set_contains(vis, vlg, phys);
+        const bool seen = set_contains_w(vis, vlg, phys, first);  // every lane must call (warp-uniform loop)
+        const bool fresh = first && !seen;
         const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fresh);
         const uint32_t rank = __popc(fm & lt);
         const bool take = fresh && rank < want - picked;
+        set_insert_w(vis, vlg, phys, take);
         if (take) {
-          set_insert(vis, vlg, phys);
           cp[picked + rank] = phys;
           cs[picked + rank] = slot;
         }
@@ -393,13 +468,15 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
         if (i < cnt) {
           const Attr at = ld_attr(a.attr, phys);
           slot = at.slot;
-          ok = slot < a.n_live && at.s >= lo_f && at.s <= hi_f && !set_contains(vis, vlg, phys);
+          ok = slot < a.n_live && at.s >= lo_f && at.s <= hi_f;
         }
+        const bool seen = set_contains_w(vis, vlg, phys, ok);  // every lane must call (warp-uniform loop)
+        ok = ok && !seen;
         const uint32_t msk = __ballot_sync(0xFFFFFFFFu, ok);
         const uint32_t rank = __popc(msk & lt);
         const bool take = ok && rank < want - picked;
+        set_insert_w(vis, vlg, phys, take);
         if (take) {
-          set_insert(vis, vlg, phys);
           cp[picked + rank] = phys;
           cs[picked + rank] = slot;
         }
@@ -415,25 +492,23 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
 // NC: 128-float chunks per row; EPL: gathered neighbours per lane per iteration
 // (width * K_max <= 32 * EPL).
 #ifndef GRAB_SEARCH_MINB
-#define GRAB_SEARCH_MINB 6  // 6 blocks x 4 warps: 85 registers (small spills beat 4 blocks)
+#define GRAB_SEARCH_MINB 6
 #endif
 template <int NC, int EPL>
 __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, SearchShape sh) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = lane_id();
+  const uint32_t lt = (1u << lane) - 1;
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t wpb = blockDim.x >> 5;
-  const WarpLayout lay = warp_layout(sh);
-  uint8_t* base = smem + wib * lay.bytes;
-  double* qd = (double*)(base + lay.qd);
-  uint32_t* qs = (uint32_t*)(base + lay.qs);
-  uint32_t* qp = (uint32_t*)(base + lay.qp);
-  uint8_t* qf = base + lay.qf;
-  double* cd = (double*)(base + lay.cd);
-  uint32_t* cs = (uint32_t*)(base + lay.cs);
-  uint32_t* cp = (uint32_t*)(base + lay.cp);
-  uint32_t* dd = (uint32_t*)(base + lay.dd);
-  uint32_t* fr = (uint32_t*)(base + lay.fr);
+  uint8_t* base = smem + wib * sh.warp_bytes;
+  uint4* qe = (uint4*)(base + sh.o_qe);
+  double* cd = (double*)(base + sh.o_cd);
+  uint32_t* cs = (uint32_t*)(base + sh.o_cs);
+  uint32_t* cp = (uint32_t*)(base + sh.o_cp);
+  uint32_t* rr = (uint32_t*)(base + sh.o_rr);
+  uint32_t* dd = (uint32_t*)(base + sh.o_dd);
+  uint32_t* fr = (uint32_t*)(base + sh.o_fr);
   const uint32_t gw = blockIdx.x * wpb + wib;
   const uint32_t vlg = sh.vlog2;
   uint32_t* vis = a.gtab + ((uint64_t)gw << vlg);
@@ -441,12 +516,14 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
   const uint32_t nw = gridDim.x * wpb;
   const uint32_t dlg = 31 - __clz(sh.dsz);
   const uint32_t K = a.k_max;
+  const uint32_t nwork = a.nwork_dev ? *a.nwork_dev : a.nwork;
 
-  for (uint32_t item = gw; item < a.nwork; item += nw) {
+  for (uint32_t item = gw; item < nwork; item += nw) {
     const uint32_t qi = a.qmap ? a.qmap[item] : item;
     const float lo_f = __double2float_rn(a.lower[(uint64_t)qi * a.range_stride]);
     const float hi_f = __double2float_rn(a.upper[(uint64_t)qi * a.range_stride]);
-    grab_search_stats st = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t iterations = 0, expanded = 0, dist_evals = 0, seed_evals = 0, attempts = 0;
+    uint32_t gath_l = 0, rej_l = 0;  // per-lane partial counts, summed at the end
     uint32_t L = 0;
     bool overflow = false;
     if (a.n_live > 0 && a.m > 0) {
@@ -457,27 +534,35 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
       const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f);
       const uint32_t hi_b = bucket_of_f32(a.bound, a.m, hi_f);
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
-      uint32_t attempts = 0;
       const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, vlg, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
-      st.seed_attempts = attempts;
+      __syncwarp();
       uint32_t vis_n = ns;
+      uint32_t fu = 0;  // every queue entry before fu is expanded
       if (ns > 0) {
         score<NC>(qr, a.X, a.dp, cp, cd, ns);
-        st.dist_evals = st.seed_evals = ns;
-        L = admit(qd, qs, qp, qf, cd, cs, cp, 0, ns, sh.itopk);
+        dist_evals = seed_evals = ns;
+        L = admit(qe, cd, cs, cp, rr, 0, ns, sh.itopk, fu);
         for (uint32_t it = 0; it < a.max_iter; ++it) {
-          // frontier: first `width` unexpanded entries
+          // frontier: first `width` unexpanded entries (searcher.py:73-79)
           uint32_t nf = 0;
-          for (uint32_t b0 = 0; b0 < L && nf < sh.width; b0 += 32) {
+          for (uint32_t b0 = fu & ~31u; b0 < L && nf < sh.width; b0 += 32) {
             const uint32_t i = b0 + lane;
-            const bool un = i < L && qf[i] == 0;
-            const uint32_t m = __ballot_sync(0xFFFFFFFFu, un);
-            const uint32_t rank = __popc(m & ((1u << lane) - 1));
-            if (un && nf + rank < sh.width) {
-              fr[nf + rank] = qp[i];
-              qf[i] = 1;
+            uint32_t w = 0;
+            bool un = false;
+            if (i < L && i >= fu) {
+              w = qe[i].w;
+              un = (w & kExpanded) == 0;
             }
-            nf = min(sh.width, nf + __popc(m));
+            const uint32_t m = __ballot_sync(kFull, un);
+            const uint32_t rank = __popc(m & lt);
+            const bool pick = un && nf + rank < sh.width;
+            if (pick) {
+              fr[nf + rank] = w;
+              qe[i].w = w | kExpanded;
+            }
+            const uint32_t pm = __ballot_sync(kFull, pick);
+            if (pm) fu = b0 + 32 - __clz(pm);  // one past the last picked entry
+            nf += __popc(pm);
           }
           __syncwarp();
           if (nf == 0) break;
@@ -486,45 +571,38 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
             overflow = true;
             break;
           }
-          st.iterations++;
-          st.expanded += nf;
+          iterations++;
+          expanded += nf;
           clear_words(dd, sh.dsz);
-          // (1) all adjacency entries of the frontier rows
+          // (1) adjacency entries of the frontier rows + their {scalar, slot}
           uint32_t v[EPL];
+          uint2 at[EPL];
 #pragma unroll
           for (int t = 0; t < EPL; ++t) {
             const uint32_t e = lane + 32 * t;
             v[t] = kSentinel;
-            if (e < fan) v[t] = __ldg(a.adj + (uint64_t)fr[e / K] * K + (e % K));
-          }
-          // (2) all Attr{scalar, slot}
-          float sv[EPL];
-          uint32_t sl[EPL];
-#pragma unroll
-          for (int t = 0; t < EPL; ++t) {
-            sl[t] = kNoSlot;
-            sv[t] = 0.f;
-            if (v[t] != kSentinel) {
-              const Attr at = ld_attr(a.attr, v[t]);
-              sl[t] = at.slot;
-              sv[t] = at.s;
+            at[t] = make_uint2(0x7FC00000u, kNoSlot);
+            if (e < fan) {
+              const uint64_t idx = (uint64_t)fr[e / K] * K + (e % K);
+              v[t] = __ldg(a.adj + idx);
+              at[t] = __ldg(reinterpret_cast<const uint2*>(a.adja) + idx);
             }
           }
           __syncwarp();
-          // (3) per-iteration unique (shared), pre-check, (4) visited CAS (global)
-          uint32_t uniq_bits = 0, cand_bits = 0, rej_bits = 0;
+          // (2) drop SENTINEL / slot >= n, per-iteration unique, scalar pre-check
+          uint32_t cand_bits = 0;
 #pragma unroll
           for (int t = 0; t < EPL; ++t) {
-            if (sl[t] < a.n_live && set_insert(dd, dlg, v[t])) {
-              uniq_bits |= 1u << t;
-              if (sv[t] >= lo_f && sv[t] <= hi_f)
-                cand_bits |= 1u << t;
-              else
-                rej_bits |= 1u << t;
-            }
+            const bool uq = set_insert_w(dd, dlg, v[t], at[t].y < a.n_live);
+            const float sv = __uint_as_float(at[t].x);
+            const bool inr = sv >= lo_f && sv <= hi_f;
+            gath_l += uq;
+            rej_l += uq && !inr;
+            cand_bits |= (uq && inr) ? 1u << t : 0u;
           }
+          __syncwarp();
+          // (3) exact visited set: every first-probe CAS of the iteration in flight at once
           {
-            // issue every first-probe CAS of the iteration before consuming any
             const uint32_t vmask = (1u << vlg) - 1;
             uint32_t h[EPL], cur[EPL];
 #pragma unroll
@@ -532,44 +610,49 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
               h[t] = hash32(v[t]) >> (32 - vlg);
               cur[t] = ((cand_bits >> t) & 1u) ? atomicCAS(vis + h[t], 0u, v[t] + 1) : 0u;
             }
+            uint32_t pend = 0;  // rare collisions: probe on, warp-uniformly
 #pragma unroll
-            for (int t = 0; t < EPL; ++t) {
-              if ((cand_bits >> t) & 1u) {
-                while (cur[t] != 0u && cur[t] != v[t] + 1) {  // rare collision: probe on
+            for (int t = 0; t < EPL; ++t)
+              pend |= (((cand_bits >> t) & 1u) && cur[t] != 0u && cur[t] != v[t] + 1) ? 1u << t : 0u;
+            while (__any_sync(kFull, pend != 0u)) {
+#pragma unroll
+              for (int t = 0; t < EPL; ++t) {
+                if ((pend >> t) & 1u) {
                   h[t] = (h[t] + 1) & vmask;
                   cur[t] = atomicCAS(vis + h[t], 0u, v[t] + 1);
+                  if (cur[t] == 0u || cur[t] == v[t] + 1) pend &= ~(1u << t);
                 }
-                if (cur[t] != 0u) cand_bits &= ~(1u << t);
               }
             }
+#pragma unroll
+            for (int t = 0; t < EPL; ++t)
+              if (cur[t] != 0u) cand_bits &= ~(1u << t);
           }
-          // (5) compact candidates in gather order + stats
+          __syncwarp();
+          // (4) compact candidates in gather order
           uint32_t nc = 0;
 #pragma unroll
           for (int t = 0; t < EPL; ++t) {
             const bool c = (cand_bits >> t) & 1u;
-            const uint32_t cm = __ballot_sync(0xFFFFFFFFu, c);
-            st.gathered += __popc(__ballot_sync(0xFFFFFFFFu, (uniq_bits >> t) & 1u));
-            st.precheck_rejected += __popc(__ballot_sync(0xFFFFFFFFu, (rej_bits >> t) & 1u));
+            const uint32_t cm = __ballot_sync(kFull, c);
             if (c) {
-              const uint32_t pos = nc + __popc(cm & ((1u << lane) - 1));
+              const uint32_t pos = nc + __popc(cm & lt);
               cp[pos] = v[t];
-              cs[pos] = sl[t];
+              cs[pos] = at[t].y;
             }
             nc += __popc(cm);
           }
           __syncwarp();
           vis_n += nc;
           if (nc == 0) continue;
-          st.in_range_new += nc;
-          st.dist_evals += nc;
+          dist_evals += nc;
           score<NC>(qr, a.X, a.dp, cp, cd, nc);
-          L = admit(qd, qs, qp, qf, cd, cs, cp, L, nc, sh.itopk);
+          L = admit(qe, cd, cs, cp, rr, L, nc, sh.itopk, fu);
         }
       }
     }
     if (overflow) {
-      if (lane == 0) {
+      if (lane == 0 && a.ovf_count) {
         const uint32_t pos = atomicAdd(a.ovf_count, 1u);
         a.ovf_list[pos] = qi;
       }
@@ -578,15 +661,67 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
     }
     const uint32_t cnt = min(L, a.k);
     for (uint32_t i = lane; i < a.k; i += 32) {
-      a.out_slots[(uint64_t)qi * a.k + i] = i < cnt ? (int64_t)qs[i] : -1;
-      a.out_dists[(uint64_t)qi * a.k + i] = i < cnt ? qd[i] : __longlong_as_double(0x7FF8000000000000ll);
+      int64_t s = -1;
+      double d = __longlong_as_double(0x7FF8000000000000ll);
+      if (i < cnt) {
+        const uint4 e = qe[i];
+        s = (int64_t)e.z;
+        d = qe_dist(e);
+      }
+      a.out_slots[(uint64_t)qi * a.k + i] = s;
+      a.out_dists[(uint64_t)qi * a.k + i] = d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gath_l += __shfl_xor_sync(kFull, gath_l, o);
+      rej_l += __shfl_xor_sync(kFull, rej_l, o);
     }
     if (lane == 0) {
       a.out_counts[qi] = cnt;
-      if (a.out_stats) a.out_stats[qi] = st;
+      if (a.out_stats) {
+        grab_search_stats st;
+        st.iterations = iterations;
+        st.dist_evals = dist_evals;
+        st.seed_evals = seed_evals;
+        st.gathered = gath_l;
+        st.in_range_new = dist_evals - seed_evals;
+        st.precheck_rejected = rej_l;
+        st.seed_attempts = attempts;
+        st.expanded = expanded;
+        a.out_stats[qi] = st;
+      }
     }
     __syncwarp();
   }
+}
+
+// adja[i] = attr[adj[i]] ({NaN, kNoSlot} for SENTINEL)
+__global__ void k_fill_adja(const uint32_t* __restrict__ adj, const Attr* __restrict__ attr, uint64_t n,
+                            uint2* __restrict__ out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t v = adj[i];
+  out[i] = v == kSentinel ? make_uint2(0x7FC00000u, kNoSlot) : __ldg(reinterpret_cast<const uint2*>(attr) + v);
+}
+
+void ensure_adja(const DevIndex& ix, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(*ix.adja_mu);
+  if (ix.adja && ix.adja_rows == ix.phys_cap && ix.adja_version == ix.adj_version) return;
+  const uint64_t n = ix.phys_cap * ix.params.k_max;
+  if (!ix.adja || ix.adja_rows != ix.phys_cap) {
+    if (ix.adja) {
+      GRAB_CUDA(cudaStreamSynchronize(st));
+      cudaFree(ix.adja);
+      ix.adja = nullptr;
+    }
+    GRAB_CUDA(cudaMalloc(&ix.adja, std::max<uint64_t>(n, 1) * sizeof(Attr)));
+    ix.adja_rows = ix.phys_cap;
+  }
+  if (n) {
+    k_fill_adja<<<(unsigned)div_up(n, 256), 256, 0, st>>>(ix.adj, ix.attr, n, reinterpret_cast<uint2*>(ix.adja));
+    GRAB_CHECK_LAUNCH();
+  }
+  ix.adja_version = ix.adj_version;
 }
 
 // ---------------------------------------------------------------- host
@@ -609,10 +744,18 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
     const uint64_t bound = (uint64_t)want + (uint64_t)max_iter * fan + fan;
     s.vlog2 = std::max<uint32_t>(11, ceil_log2(bound * 4 / 3 + 1));
   }
+  const WarpLayout l = warp_layout(s);
+  s.o_qe = l.qe;
+  s.o_cd = l.cd;
+  s.o_cs = l.cs;
+  s.o_cp = l.cp;
+  s.o_rr = l.rr;
+  s.o_dd = l.dd;
+  s.o_fr = l.fr;
+  s.warp_bytes = l.bytes;
   return s;
 }
 
-// returns the number of warps the grid runs (for sizing the visited tables)
 template <int NC, int EPL>
 static void launch_t(const SearchArgs& a, const SearchShape& sh, uint32_t wpb, uint32_t blocks, uint32_t smem,
                      cudaStream_t st) {
@@ -650,7 +793,10 @@ static int occupancy_blocks(uint32_t nc, uint32_t epl, uint32_t wpb, uint32_t sm
   return per_sm < 1 ? 1 : per_sm;
 }
 
-static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_t st, DBufLite& tables) {
+// Launches one search grid: min(work, resident capacity) blocks of 4 warps,
+// `max_blocks` caps the grid (worst-case retry: bounded table memory).
+static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_t st, DBufLite& tables,
+                   uint64_t max_blocks) {
   const WarpLayout lay = warp_layout(sh);
   const uint32_t wpb = 4;
   const uint32_t smem = lay.bytes * wpb;
@@ -662,7 +808,8 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   epl = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
   if (epl > 4 || sh.cmax > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
   const int per_sm = occupancy_blocks(nc, epl, wpb, smem);
-  const uint64_t blocks = std::min<uint64_t>(div_up(a.nwork, wpb), (uint64_t)per_sm * num_sms);
+  const uint64_t blocks =
+      std::min<uint64_t>(std::min<uint64_t>(div_up(a.nwork, wpb), (uint64_t)per_sm * num_sms), max_blocks);
   if (!blocks) return;
   // one visited table per resident warp
   const uint64_t words = blocks * wpb * (1ull << sh.vlog2);
@@ -678,37 +825,38 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
     dispatch_epl<8>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
 }
 
+// Stream-ordered and host-sync free: queries whose visited table would pass
+// 3/4 load are listed by the main grid and re-run exactly by a second grid with
+// a worst-case table; that grid reads its work count on the device (and exits
+// at once when nothing overflowed).
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
   if (a.width * a.k_max > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
+  if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
+  ensure_adja(ix, st);
+  a.adja = ix.adja;
   SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false);
-  DBufLite tables, ovfb;
+  DBufLite tables, big_tables, ovfb;
   ovfb.ensure((a.nwork + 1) * sizeof(uint32_t), st);
   uint32_t* ovf = (uint32_t*)ovfb.p;
   GRAB_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
   a.ovf_count = ovf;
   a.ovf_list = ovf + 1;
   a.qmap = nullptr;
-  launch(a, sh, ix.num_sms, st, tables);
-  uint32_t n_ovf = 0;
-  GRAB_CUDA(cudaMemcpyAsync(&n_ovf, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  GRAB_CUDA(cudaStreamSynchronize(st));
-  if (getenv("GRAB_DEBUG")) fprintf(stderr, "[grab] search nwork=%u vlog2=%u overflow=%u\n", a.nwork, sh.vlog2, n_ovf);
-  if (n_ovf) {
-    // exact re-run of the overflowed queries with a worst-case visited table
-    SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true);
-    SearchArgs b = a;
-    DBufLite qm;
-    qm.ensure(n_ovf * sizeof(uint32_t), st);
-    GRAB_CUDA(cudaMemcpyAsync(qm.p, a.ovf_list, n_ovf * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-    b.qmap = (const uint32_t*)qm.p;
-    b.nwork = n_ovf;
-    GRAB_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
-    launch(b, big, ix.num_sms, st, tables);
-    uint32_t again = 0;
-    GRAB_CUDA(cudaMemcpyAsync(&again, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  a.nwork_dev = nullptr;
+  launch(a, sh, ix.num_sms, st, tables, ~0ull);
+  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true);
+  SearchArgs b = a;
+  b.qmap = a.ovf_list;
+  b.nwork_dev = ovf;
+  b.ovf_count = nullptr;  // cannot overflow: the table bounds every insert of max_iter iterations
+  b.ovf_list = nullptr;
+  launch(b, big, ix.num_sms, st, big_tables, (uint64_t)ix.num_sms);
+  if (getenv("GRAB_DEBUG")) {
+    uint32_t n_ovf = 0;
+    GRAB_CUDA(cudaMemcpyAsync(&n_ovf, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     GRAB_CUDA(cudaStreamSynchronize(st));
-    if (again) throw Error(GRAB_ERR_CUDA, "visited-set overflow persisted on the worst-case retry");
+    fprintf(stderr, "[grab] search nwork=%u vlog2=%u overflow=%u\n", a.nwork, sh.vlog2, n_ovf);
   }
 }
 

@@ -11,6 +11,7 @@ struct SearchArgs {
   const float* X;
   const Attr* attr;
   const uint32_t* adj;
+  const Attr* adja;  // per-adjacency-entry {scalar, slot} (DevIndex::adja)
   uint32_t dp, k_max;
   const float* bound;
   uint32_t m;
@@ -30,6 +31,7 @@ struct SearchArgs {
   // work list / overflow retry
   const uint32_t* qmap;
   uint32_t nwork;
+  const uint32_t* nwork_dev;  // if set, the work count is read on the device
   uint32_t* gtab;
   uint32_t* ovf_list;
   uint32_t* ovf_count;
@@ -42,6 +44,8 @@ struct SearchArgs {
 
 struct SearchShape {
   uint32_t itopk, width, cmax, dsz, vlog2;
+  // per-warp shared-memory layout (byte offsets, filled by make_shape)
+  uint32_t o_qe, o_cd, o_cs, o_cp, o_rr, o_dd, o_fr, warp_bytes;
 };
 
 SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst);

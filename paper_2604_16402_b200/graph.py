@@ -88,8 +88,9 @@ class GraphIndex:
     # -- lifecycle ---------------------------------------------------------
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            L.lib.grab_destroy(h)
+        lib = getattr(L, "lib", None) if L is not None else None
+        if h is not None and h.value and lib is not None:  # (module globals may be gone at interpreter exit)
+            lib.grab_destroy(h)
             self._h = None
 
     @property

@@ -8,6 +8,6 @@ for MB in ${MINBS:-4 5 6}; do
      --expt-relaxed-constexpr -DGRAB_SEARCH_MINB=$MB -c search.cu -o build/search.o && \
    nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../libgrab.so $(ls *.cu | sed 's/\.cu$/.o/; s/^/build\//'))
   echo "MINB=$MB"
-  python tools/profile_search.py --config cfg2 --reps 5 --time --points "${POINTS:-128:4:50,256:4:100}" 2>&1 | tail -2
+  python tools/search_lab.py --config cfg2 --reps 10 --points "${POINTS:-224:4:100,128:4:50}" 2>&1 | grep -v "^ "
 done
 touch $C/search.cu
