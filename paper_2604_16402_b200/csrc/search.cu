@@ -116,7 +116,7 @@ __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
   l.cs = o;
   o += align16(s.cmax * 4);
   l.cp = o;
-  o += align16(s.cmax * 4);
+  o += align16((s.cmax + 8) * 4);
   l.rr = o;
   o += align16(s.cmax * 4);
   l.dd = o;
@@ -156,8 +156,11 @@ struct GroupOf {
 };
 
 // Distances for cand[0..n): writes cd[i]. All lanes participate; G rows are in
-// flight per round (16-byte ld.global.nc per lane per 128-float chunk).
-template <int NC>
+// flight per round (16-byte ld.global.nc per lane per 128-float chunk). The
+// caller pads cp[n .. n+G) with a valid row id, so every round issues G
+// unconditional loads (results past n are discarded). FULL: dp == 128*NC (no
+// lane sits past the row end); otherwise every chunk load is predicated.
+template <int NC, bool FULL>
 __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __restrict__ X, uint32_t dp,
                                       const uint32_t* cp, double* cd, uint32_t n) {
   constexpr int G = GroupOf<NC>::G;
@@ -167,13 +170,13 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
     float4 x[G][NC];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const uint32_t i = base + g;
-      const uint32_t p = cp[i < n ? i : base];
-      const float* row = X + (uint64_t)p * dp;
+      const float* row = X + (uint64_t)cp[base + g] * dp + lane * 4;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        const uint32_t col = (c * 32 + lane) * 4;
-        x[g][c] = col < dp ? ldg_nc_f4(row + col) : make_float4(0, 0, 0, 0);
+        if (FULL)
+          x[g][c] = ldg_nc_f4(row + c * 128);
+        else
+          x[g][c] = (c * 32 + lane) * 4 < dp ? ldg_nc_f4(row + c * 128) : make_float4(0, 0, 0, 0);
       }
     }
     double part[G];
@@ -184,7 +187,6 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
       for (int c = 0; c < NC; ++c) acc = sq4(x[g][c], qr.q[c], acc);
       part[g] = acc;
     }
-    __syncwarp();
     const double v = reduce_scatter<G>(part);
     constexpr uint32_t SPAN = 32 / G;  // lanes holding each candidate's sum
     const uint32_t g = lane / SPAN;
@@ -193,41 +195,16 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
   __syncwarp();
 }
 
-// ---------------------------------------------------------------- queue ops
-// Shared-memory bitonic sort of (d, s, p)[0..n) padded to P (power of 2); used
-// only when more than 32 candidates survive (queue filling up).
-__device__ __forceinline__ void bitonic_sort(double* d, uint32_t* s, uint32_t* p, uint32_t n, uint32_t P) {
-  const uint32_t lane = lane_id();
-  for (uint32_t i = n + lane; i < P; i += 32) {
-    d[i] = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-    s[i] = kFull;
-    p[i] = kFull;
-  }
+// Pad cp[n .. n+8) with cp[0] so score() can issue whole rounds.
+__device__ __forceinline__ void pad_cands(uint32_t* cp, uint32_t n) {
   __syncwarp();
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < P; i += 32) {
-        const uint32_t l = i ^ j;
-        if (l > i) {
-          const double di = d[i], dl = d[l];
-          const uint32_t si = s[i], sl = s[l];
-          const bool asc = (i & k) == 0;
-          if (key_less(dl, sl, di, si) == asc) {
-            d[i] = dl;
-            d[l] = di;
-            s[i] = sl;
-            s[l] = si;
-            const uint32_t t = p[i];
-            p[i] = p[l];
-            p[l] = t;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
+  const uint32_t lane = lane_id();
+  const uint32_t p0 = cp[0];
+  if (lane < 8) cp[n + lane] = p0;
+  __syncwarp();
 }
 
+// ---------------------------------------------------------------- queue ops
 // Register bitonic sort of one (d, s, p) per lane, ascending across lanes.
 __device__ __forceinline__ void warp_sort32(double& d, uint32_t& s, uint32_t& p) {
   const uint32_t lane = lane_id();
@@ -276,104 +253,62 @@ __device__ __forceinline__ uint32_t upper_rank(const uint32_t* rr, uint32_t n, u
 }
 
 // CandidateQueue.admit (searcher.py:64-71): merge the nc candidates (cd, cs,
-// cp) into the queue of length L in place, truncated to itopk. Candidates that
-// cannot survive truncation are dropped first; the survivors are sorted (in
-// registers when <= 32), ranked against the queue by binary search, and every
-// displaced queue entry moves once. `fu` (first-unexpanded hint) is lowered to
-// the first new entry. Returns the new length.
-__device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, uint32_t* cp, uint32_t* rr, uint32_t L,
-                                          uint32_t nc, uint32_t itopk, uint32_t& fu) {
+// cp) into the queue of length L in place, truncated to itopk, 32 candidates
+// at a time (merging chunk by chunk with truncation after each equals one
+// merge of the union). Per chunk: candidates that cannot beat the current
+// tail are dropped, the rest are sorted in registers, ranked against the queue
+// by binary search, and every displaced queue entry moves once. `fu` (first-
+// unexpanded hint) is lowered to the first new entry. Returns the new length.
+__device__ __forceinline__ uint32_t admit(uint4* qe, const double* cd, const uint32_t* cs, const uint32_t* cp,
+                                          uint32_t* rr, uint32_t L, uint32_t nc, uint32_t itopk, uint32_t& fu) {
   const uint32_t lane = lane_id();
-  if (L == itopk && nc) {
-    const uint4 te = qe[L - 1];
-    const double td = qe_dist(te);
-    const uint32_t ts = te.z;
-    uint32_t kept = 0;
-    for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
-      const uint32_t i = b0 + lane;
-      bool ok = false;
-      double d = 0;
-      uint32_t s = 0, p = 0;
-      if (i < nc) {
-        d = cd[i];
-        s = cs[i];
-        p = cp[i];
-        ok = key_less(d, s, td, ts);
-      }
-      const uint32_t m = __ballot_sync(kFull, ok);
-      __syncwarp();
-      if (ok) {
-        const uint32_t pos = kept + __popc(m & ((1u << lane) - 1));
-        cd[pos] = d;
-        cs[pos] = s;
-        cp[pos] = p;
-      }
-      kept += __popc(m);
-      __syncwarp();
-    }
-    nc = kept;
-  }
-  if (nc == 0) return L;
   const double kInf = __longlong_as_double(0x7FF0000000000000ll);
-  if (nc <= 32) {
+  for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
+    const uint32_t i = b0 + lane;
     double d = kInf;
     uint32_t s = kFull, p = kFull;
-    if (lane < nc) {
-      d = cd[lane];
-      s = cs[lane];
-      p = cp[lane];
+    bool ok = i < nc;
+    if (ok) {
+      d = cd[i];
+      s = cs[i];
+      p = cp[i];
     }
-    warp_sort32(d, s, p);
+    if (L == itopk) {
+      const uint4 te = qe[L - 1];
+      ok = ok && key_less(d, s, qe_dist(te), te.z);
+    }
+    const uint32_t cnt = __popc(__ballot_sync(kFull, ok));
+    if (cnt == 0) continue;
+    if (!ok) {
+      d = kInf;
+      s = kFull;
+      p = kFull;
+    }
+    warp_sort32(d, s, p);  // survivors first, +inf pads last
     const uint32_t r = rank_in_queue(qe, L, d, s);
     rr[lane] = r;
     __syncwarp();
     const uint32_t r0 = __shfl_sync(kFull, r, 0);
     if (r0 < L) {
-      for (int32_t b0 = (int32_t)((L - 1) & ~31u); b0 >= (int32_t)(r0 & ~31u); b0 -= 32) {
-        const uint32_t i = (uint32_t)b0 + lane;
+      for (int32_t c0 = (int32_t)((L - 1) & ~31u); c0 >= (int32_t)(r0 & ~31u); c0 -= 32) {
+        const uint32_t j = (uint32_t)c0 + lane;
         uint4 e;
         uint32_t dst = kFull;
-        if (i < L && i >= r0) {
-          e = qe[i];
-          dst = i + upper_rank(rr, nc, i);
+        if (j < L && j >= r0) {
+          e = qe[j];
+          dst = j + upper_rank(rr, cnt, j);
         }
         __syncwarp();
         if (dst < itopk) qe[dst] = e;
         __syncwarp();
       }
     }
-    const uint32_t pos = lane + r;
-    if (lane < nc && pos < itopk) qe[pos] = qe_pack(d, s, p);
+    if (lane < cnt && lane + r < itopk) qe[lane + r] = qe_pack(d, s, p);
     fu = min(fu, r0);
-  } else {
-    uint32_t P = 64;
-    while (P < nc) P <<= 1;
-    bitonic_sort(cd, cs, cp, nc, P);
-    for (uint32_t j = lane; j < nc; j += 32) rr[j] = rank_in_queue(qe, L, cd[j], cs[j]);
+    L = min(itopk, L + cnt);
     __syncwarp();
-    const uint32_t r0 = rr[0];
-    if (r0 < L) {
-      for (int32_t b0 = (int32_t)((L - 1) & ~31u); b0 >= (int32_t)(r0 & ~31u); b0 -= 32) {
-        const uint32_t i = (uint32_t)b0 + lane;
-        uint4 e;
-        uint32_t dst = kFull;
-        if (i < L && i >= r0) {
-          e = qe[i];
-          dst = i + upper_rank(rr, nc, i);
-        }
-        __syncwarp();
-        if (dst < itopk) qe[dst] = e;
-        __syncwarp();
-      }
-    }
-    for (uint32_t j = lane; j < nc; j += 32) {
-      const uint32_t pos = j + rr[j];
-      if (pos < itopk) qe[pos] = qe_pack(cd[j], cs[j], cp[j]);
-    }
-    fu = min(fu, r0);
   }
-  __syncwarp();
-  return min(itopk, L + nc);
+  return L;
 }
 
 // ---------------------------------------------------------------- seeds
@@ -494,7 +429,7 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
 #ifndef GRAB_SEARCH_MINB
 #define GRAB_SEARCH_MINB 6
 #endif
-template <int NC, int EPL>
+template <int NC, int EPL, bool FULL>
 __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, SearchShape sh) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = lane_id();
@@ -539,7 +474,8 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
       uint32_t vis_n = ns;
       uint32_t fu = 0;  // every queue entry before fu is expanded
       if (ns > 0) {
-        score<NC>(qr, a.X, a.dp, cp, cd, ns);
+        pad_cands(cp, ns);
+        score<NC, FULL>(qr, a.X, a.dp, cp, cd, ns);
         dist_evals = seed_evals = ns;
         L = admit(qe, cd, cs, cp, rr, 0, ns, sh.itopk, fu);
         for (uint32_t it = 0; it < a.max_iter; ++it) {
@@ -646,7 +582,8 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           vis_n += nc;
           if (nc == 0) continue;
           dist_evals += nc;
-          score<NC>(qr, a.X, a.dp, cp, cd, nc);
+          pad_cands(cp, nc);
+          score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc);
           L = admit(qe, cd, cs, cp, rr, L, nc, sh.itopk, fu);
         }
       }
@@ -756,41 +693,21 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   return s;
 }
 
-template <int NC, int EPL>
-static void launch_t(const SearchArgs& a, const SearchShape& sh, uint32_t wpb, uint32_t blocks, uint32_t smem,
-                     cudaStream_t st) {
-  auto kern = k_search<NC, EPL>;
-  GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<blocks, 32 * wpb, smem, st>>>(a, sh);
-  GRAB_CHECK_LAUNCH();
-}
-
-template <int NC>
-static void dispatch_epl(uint32_t epl, const SearchArgs& a, const SearchShape& sh, uint32_t wpb, uint32_t blocks,
-                         uint32_t smem, cudaStream_t st) {
-  if (epl <= 1)
-    launch_t<NC, 1>(a, sh, wpb, blocks, smem, st);
-  else if (epl <= 2)
-    launch_t<NC, 2>(a, sh, wpb, blocks, smem, st);
-  else if (epl <= 4)
-    launch_t<NC, 4>(a, sh, wpb, blocks, smem, st);
-  else
-    throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
-}
-
-static int occupancy_blocks(uint32_t nc, uint32_t epl, uint32_t wpb, uint32_t smem) {
-  int per_sm = 0;
-  auto q = [&](auto kern) {
-    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
-  };
-  // occupancy depends on registers (template) and smem; probe the instance that will run
-#define GRAB_Q(NC_, EPL_) \
-  if (nc == NC_ && epl == EPL_) q(k_search<NC_, EPL_>);
-  GRAB_Q(1, 1) GRAB_Q(1, 2) GRAB_Q(1, 4) GRAB_Q(2, 1) GRAB_Q(2, 2) GRAB_Q(2, 4) GRAB_Q(4, 1) GRAB_Q(4, 2)
-  GRAB_Q(4, 4) GRAB_Q(8, 1) GRAB_Q(8, 2) GRAB_Q(8, 4)
-#undef GRAB_Q
-  return per_sm < 1 ? 1 : per_sm;
+// Calls f(kernel) with the k_search instance for (nc, epl, full).
+template <typename F>
+static void with_kernel(uint32_t nc, uint32_t epl, bool full, F&& f) {
+#define GRAB_K(NC_, EPL_)                      \
+  if (nc == NC_ && epl == EPL_) {              \
+    if (full)                                  \
+      f(k_search<NC_, EPL_, true>);            \
+    else                                       \
+      f(k_search<NC_, EPL_, false>);           \
+    return;                                    \
+  }
+  GRAB_K(1, 1) GRAB_K(1, 2) GRAB_K(1, 4) GRAB_K(2, 1) GRAB_K(2, 2) GRAB_K(2, 4)
+  GRAB_K(4, 1) GRAB_K(4, 2) GRAB_K(4, 4) GRAB_K(8, 1) GRAB_K(8, 2) GRAB_K(8, 4)
+#undef GRAB_K
+  throw Error(GRAB_ERR_VALUE, "unsupported search kernel shape");
 }
 
 // Launches one search grid: min(work, resident capacity) blocks of 4 warps,
@@ -807,7 +724,13 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   uint32_t epl = (uint32_t)div_up(sh.width * a.k_max, 32);
   epl = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
   if (epl > 4 || sh.cmax > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
-  const int per_sm = occupancy_blocks(nc, epl, wpb, smem);
+  const bool full = a.dp == nc * 128;
+  int per_sm = 1;
+  with_kernel(nc, epl, full, [&](auto kern) {
+    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
+  });
+  per_sm = std::max(per_sm, 1);
   const uint64_t blocks =
       std::min<uint64_t>(std::min<uint64_t>(div_up(a.nwork, wpb), (uint64_t)per_sm * num_sms), max_blocks);
   if (!blocks) return;
@@ -815,14 +738,10 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   const uint64_t words = blocks * wpb * (1ull << sh.vlog2);
   tables.ensure(words * 4, st);
   a.gtab = (uint32_t*)tables.p;
-  if (nc == 1)
-    dispatch_epl<1>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
-  else if (nc == 2)
-    dispatch_epl<2>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
-  else if (nc == 4)
-    dispatch_epl<4>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
-  else
-    dispatch_epl<8>(epl, a, sh, wpb, (uint32_t)blocks, smem, st);
+  with_kernel(nc, epl, full, [&](auto kern) {
+    kern<<<(uint32_t)blocks, 32 * wpb, smem, st>>>(a, sh);
+    GRAB_CHECK_LAUNCH();
+  });
 }
 
 // Stream-ordered and host-sync free: queries whose visited table would pass
