@@ -90,6 +90,36 @@ __device__ __forceinline__ bool set_contains_w(const uint32_t* tab, uint32_t lg,
   return active && cur == v;
 }
 
+// Exact per-query visited set (searcher.py:90-98 epoch table). Only in-range
+// nodes are ever stamped, and every in-range node lives in the slab interval
+// [base, base + nbits) of the query's bucket interval, so when that interval
+// fits the warp's table as a bitmap (<= 32 * 2^lg rows) the set is a bitmap:
+// one atomicOr per insert, no probing, and only nbits/8 bytes to clear and to
+// keep in L2. Wider intervals (e.g. full-range insert searches) use the
+// open-addressing hash table.
+struct Visited {
+  uint32_t* tab;
+  uint32_t lg, base, nbits;
+  bool bm;
+  __device__ __forceinline__ uint32_t clear_words_n() const {
+    return bm ? ((nbits + 4095u) >> 12) << 7 : (1u << lg);  // multiple of 128 words
+  }
+  __device__ __forceinline__ bool contains_w(uint32_t key, bool active) const {
+    if (bm) {
+      const uint32_t o = key - base;
+      return active && (*((volatile const uint32_t*)(tab + (o >> 5))) >> (o & 31) & 1u);
+    }
+    return set_contains_w(tab, lg, key, active);
+  }
+  __device__ __forceinline__ bool insert_w(uint32_t key, bool active) const {
+    if (bm) {
+      const uint32_t o = key - base;
+      return active && !(atomicOr(tab + (o >> 5), 1u << (o & 31)) >> (o & 31) & 1u);
+    }
+    return set_insert_w(tab, lg, key, active);
+  }
+};
+
 __device__ __forceinline__ void clear_words(uint32_t* p, uint32_t n) {
   // n is a multiple of 128 (4 words per lane per step)
   const uint4 z = make_uint4(0, 0, 0, 0);
@@ -118,7 +148,7 @@ __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
   l.cp = o;
   o += align16((s.cmax + 8) * 4);
   l.rr = o;
-  o += align16(s.cmax * 4);
+  o += 32 * 4;
   l.dd = o;
   o += align16(s.dsz * 4);
   l.fr = o;
@@ -152,7 +182,10 @@ __device__ __forceinline__ void load_query(QueryRegs<NC>& r, const float* q, uin
 
 template <int NC>
 struct GroupOf {
-  static constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : (NC <= 4 ? 2 : 1));
+#ifndef GRAB_SEARCH_G1
+#define GRAB_SEARCH_G1 8
+#endif
+  static constexpr int G = NC == 1 ? GRAB_SEARCH_G1 : (NC == 2 ? 4 : (NC <= 4 ? 2 : 1));
 };
 
 // Distances for cand[0..n): writes cd[i]. All lanes participate; G rows are in
@@ -195,6 +228,15 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
   __syncwarp();
 }
 
+// Pull every candidate row toward L2 at once (one bulk prefetch per lane per
+// row, no registers held), so score()'s G-row rounds hit L2 instead of HBM.
+__device__ __forceinline__ void prefetch_rows(const float* X, uint32_t dp, const uint32_t* cp, uint32_t n) {
+  for (uint32_t i = lane_id(); i < n; i += 32) {
+    const float* row = X + (uint64_t)cp[i] * dp;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"(dp * 4) : "memory");
+  }
+}
+
 // Pad cp[n .. n+8) with cp[0] so score() can issue whole rounds.
 __device__ __forceinline__ void pad_cands(uint32_t* cp, uint32_t n) {
   __syncwarp();
@@ -205,12 +247,13 @@ __device__ __forceinline__ void pad_cands(uint32_t* cp, uint32_t n) {
 }
 
 // ---------------------------------------------------------------- queue ops
-// Register bitonic sort of one (d, s, p) per lane, ascending across lanes.
-__device__ __forceinline__ void warp_sort32(double& d, uint32_t& s, uint32_t& p) {
+// Register bitonic sort of one (d, s, p) per lane, ascending across lanes
+// [0, S) for S = 2^lgS (lanes >= S are sorted among themselves; callers put
+// +inf pads there).
+__device__ __forceinline__ void warp_sort(double& d, uint32_t& s, uint32_t& p, uint32_t lgS) {
   const uint32_t lane = lane_id();
-#pragma unroll
-  for (uint32_t k = 2; k <= 32; k <<= 1) {
-#pragma unroll
+  for (uint32_t k = 2; k <= (1u << lgS); k <<= 1) {
+#pragma unroll 5
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       const double od = __shfl_xor_sync(kFull, d, j);
       const uint32_t os = __shfl_xor_sync(kFull, s, j);
@@ -253,16 +296,45 @@ __device__ __forceinline__ uint32_t upper_rank(const uint32_t* rr, uint32_t n, u
 }
 
 // CandidateQueue.admit (searcher.py:64-71): merge the nc candidates (cd, cs,
-// cp) into the queue of length L in place, truncated to itopk, 32 candidates
-// at a time (merging chunk by chunk with truncation after each equals one
-// merge of the union). Per chunk: candidates that cannot beat the current
-// tail are dropped, the rest are sorted in registers, ranked against the queue
-// by binary search, and every displaced queue entry moves once. `fu` (first-
-// unexpanded hint) is lowered to the first new entry. Returns the new length.
-__device__ __forceinline__ uint32_t admit(uint4* qe, const double* cd, const uint32_t* cs, const uint32_t* cp,
-                                          uint32_t* rr, uint32_t L, uint32_t nc, uint32_t itopk, uint32_t& fu) {
+// cp) into the queue of length L in place, truncated to itopk. Candidates that
+// cannot beat the current tail are dropped first (compacted in place); the
+// survivors are merged 32 at a time (chunk by chunk with truncation after each
+// equals one merge of the union): sorted in registers (network sized to the
+// chunk), ranked against the queue by binary search, and every displaced
+// queue entry moves once. `fu` (first-unexpanded hint) is lowered to the first
+// new entry. Returns the new length.
+__device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, uint32_t* cp, uint32_t* rr, uint32_t L,
+                                          uint32_t nc, uint32_t itopk, uint32_t& fu) {
   const uint32_t lane = lane_id();
   const double kInf = __longlong_as_double(0x7FF0000000000000ll);
+  if (L == itopk && nc) {
+    const uint4 te = qe[L - 1];
+    const double td = qe_dist(te);
+    uint32_t kept = 0;
+    for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
+      const uint32_t i = b0 + lane;
+      double d = 0;
+      uint32_t s = 0, p = 0;
+      bool ok = false;
+      if (i < nc) {
+        d = cd[i];
+        s = cs[i];
+        p = cp[i];
+        ok = key_less(d, s, td, te.z);
+      }
+      const uint32_t m = __ballot_sync(kFull, ok);
+      __syncwarp();
+      if (ok) {
+        const uint32_t pos = kept + __popc(m & ((1u << lane) - 1));
+        cd[pos] = d;
+        cs[pos] = s;
+        cp[pos] = p;
+      }
+      kept += __popc(m);
+    }
+    __syncwarp();
+    nc = kept;
+  }
   for (uint32_t b0 = 0; b0 < nc; b0 += 32) {
     const uint32_t i = b0 + lane;
     double d = kInf;
@@ -273,7 +345,7 @@ __device__ __forceinline__ uint32_t admit(uint4* qe, const double* cd, const uin
       s = cs[i];
       p = cp[i];
     }
-    if (L == itopk) {
+    if (b0 > 0 && L == itopk) {  // the tail moved since the prefilter
       const uint4 te = qe[L - 1];
       ok = ok && key_less(d, s, qe_dist(te), te.z);
     }
@@ -284,7 +356,9 @@ __device__ __forceinline__ uint32_t admit(uint4* qe, const double* cd, const uin
       s = kFull;
       p = kFull;
     }
-    warp_sort32(d, s, p);  // survivors first, +inf pads last
+    // survivors sit in lanes [0, navail): a network over the next power of 2 sorts them first
+    const uint32_t navail = min(32u, nc - b0);
+    warp_sort(d, s, p, navail <= 1 ? 0 : 32 - __clz(navail - 1));
     const uint32_t r = rank_in_queue(qe, L, d, s);
     rr[lane] = r;
     __syncwarp();
@@ -316,8 +390,8 @@ __device__ __forceinline__ uint32_t admit(uint4* qe, const double* cd, const uin
 // lane L owns output 32r+L = words lo,hi) are compacted into `stage` in word
 // order, then consumed 32 at a time in draw order. Returns seeds written to
 // (cp, cs)[0..n); *attempts = SearchStats.seed_attempts.
-__device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t* cp, uint32_t* cs, uint32_t* vis,
-                                 uint32_t vlg, uint32_t lo_b, uint32_t hi_b, float lo_f, float hi_f,
+__device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t* cp, uint32_t* cs, const Visited& vis,
+                                 uint32_t lo_b, uint32_t hi_b, float lo_f, float hi_f,
                                  uint64_t rng_seed, uint32_t* attempts) {
   const uint32_t lane = lane_id();
   const uint32_t lt = (1u << lane) - 1;
@@ -372,12 +446,12 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
         const bool inr = have && slot < a.n_live && sv >= lo_f && sv <= hi_f;
         const uint32_t same = __match_any_sync(0xFFFFFFFFu, inr ? phys : 0xFFFFFFFFu);
         const bool first = inr && (uint32_t)(__ffs(same) - 1) == lane;
-        const bool seen = set_contains_w(vis, vlg, phys, first);  // every lane must call (warp-uniform loop)
+        const bool seen = vis.contains_w(phys, first);  // every lane must call (warp-uniform loop)
         const bool fresh = first && !seen;
         const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fresh);
         const uint32_t rank = __popc(fm & lt);
         const bool take = fresh && rank < want - picked;
-        set_insert_w(vis, vlg, phys, take);
+        vis.insert_w(phys, take);
         if (take) {
           cp[picked + rank] = phys;
           cs[picked + rank] = slot;
@@ -405,12 +479,12 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
           slot = at.slot;
           ok = slot < a.n_live && at.s >= lo_f && at.s <= hi_f;
         }
-        const bool seen = set_contains_w(vis, vlg, phys, ok);  // every lane must call (warp-uniform loop)
+        const bool seen = vis.contains_w(phys, ok);  // every lane must call (warp-uniform loop)
         ok = ok && !seen;
         const uint32_t msk = __ballot_sync(0xFFFFFFFFu, ok);
         const uint32_t rank = __popc(msk & lt);
         const bool take = ok && rank < want - picked;
-        set_insert_w(vis, vlg, phys, take);
+        vis.insert_w(phys, take);
         if (take) {
           cp[picked + rank] = phys;
           cs[picked + rank] = slot;
@@ -446,7 +520,7 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
   uint32_t* fr = (uint32_t*)(base + sh.o_fr);
   const uint32_t gw = blockIdx.x * wpb + wib;
   const uint32_t vlg = sh.vlog2;
-  uint32_t* vis = a.gtab + ((uint64_t)gw << vlg);
+  uint32_t* vtab = a.gtab + ((uint64_t)gw << vlg);
   const uint32_t vcap = (1u << vlg) / 4 * 3;
   const uint32_t nw = gridDim.x * wpb;
   const uint32_t dlg = 31 - __clz(sh.dsz);
@@ -462,14 +536,20 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
     uint32_t L = 0;
     bool overflow = false;
     if (a.n_live > 0 && a.m > 0) {
-      clear_words(vis, 1u << vlg);
-      __syncwarp();
       QueryRegs<NC> qr;
       load_query<NC>(qr, a.qphys ? a.X + (uint64_t)a.qphys[qi] * a.dp : a.Q + (uint64_t)qi * a.dp, a.dp);
       const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f);
       const uint32_t hi_b = bucket_of_f32(a.bound, a.m, hi_f);
+      Visited vis;
+      vis.tab = vtab;
+      vis.lg = vlg;
+      vis.base = __ldg(a.bstart + lo_b);
+      vis.nbits = __ldg(a.bstart + hi_b) + __ldg(a.bcount + hi_b) - vis.base;
+      vis.bm = vis.nbits <= (32u << vlg);
+      clear_words(vtab, vis.clear_words_n());
+      __syncwarp();
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
-      const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, vlg, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
+      const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
       __syncwarp();
       uint32_t vis_n = ns;
       uint32_t fu = 0;  // every queue entry before fu is expanded
@@ -503,7 +583,7 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           __syncwarp();
           if (nf == 0) break;
           const uint32_t fan = nf * K;
-          if (vis_n + fan > vcap) {
+          if (!vis.bm && vis_n + fan > vcap) {  // (a bitmap cannot overflow)
             overflow = true;
             break;
           }
@@ -537,32 +617,44 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
             cand_bits |= (uq && inr) ? 1u << t : 0u;
           }
           __syncwarp();
-          // (3) exact visited set: every first-probe CAS of the iteration in flight at once
+          // (3) exact visited set: every first-probe atomic of the iteration in flight at once
           {
-            const uint32_t vmask = (1u << vlg) - 1;
-            uint32_t h[EPL], cur[EPL];
-#pragma unroll
-            for (int t = 0; t < EPL; ++t) {
-              h[t] = hash32(v[t]) >> (32 - vlg);
-              cur[t] = ((cand_bits >> t) & 1u) ? atomicCAS(vis + h[t], 0u, v[t] + 1) : 0u;
-            }
-            uint32_t pend = 0;  // rare collisions: probe on, warp-uniformly
-#pragma unroll
-            for (int t = 0; t < EPL; ++t)
-              pend |= (((cand_bits >> t) & 1u) && cur[t] != 0u && cur[t] != v[t] + 1) ? 1u << t : 0u;
-            while (__any_sync(kFull, pend != 0u)) {
+            uint32_t cur[EPL];
+            if (vis.bm) {
 #pragma unroll
               for (int t = 0; t < EPL; ++t) {
-                if ((pend >> t) & 1u) {
-                  h[t] = (h[t] + 1) & vmask;
-                  cur[t] = atomicCAS(vis + h[t], 0u, v[t] + 1);
-                  if (cur[t] == 0u || cur[t] == v[t] + 1) pend &= ~(1u << t);
+                const uint32_t o = v[t] - vis.base;
+                cur[t] = ((cand_bits >> t) & 1u) ? atomicOr(vtab + (o >> 5), 1u << (o & 31)) : 0u;
+              }
+#pragma unroll
+              for (int t = 0; t < EPL; ++t)
+                if ((cur[t] >> ((v[t] - vis.base) & 31)) & 1u) cand_bits &= ~(1u << t);
+            } else {
+              const uint32_t vmask = (1u << vlg) - 1;
+              uint32_t h[EPL];
+#pragma unroll
+              for (int t = 0; t < EPL; ++t) {
+                h[t] = hash32(v[t]) >> (32 - vlg);
+                cur[t] = ((cand_bits >> t) & 1u) ? atomicCAS(vtab + h[t], 0u, v[t] + 1) : 0u;
+              }
+              uint32_t pend = 0;  // rare collisions: probe on, warp-uniformly
+#pragma unroll
+              for (int t = 0; t < EPL; ++t)
+                pend |= (((cand_bits >> t) & 1u) && cur[t] != 0u && cur[t] != v[t] + 1) ? 1u << t : 0u;
+              while (__any_sync(kFull, pend != 0u)) {
+#pragma unroll
+                for (int t = 0; t < EPL; ++t) {
+                  if ((pend >> t) & 1u) {
+                    h[t] = (h[t] + 1) & vmask;
+                    cur[t] = atomicCAS(vtab + h[t], 0u, v[t] + 1);
+                    if (cur[t] == 0u || cur[t] == v[t] + 1) pend &= ~(1u << t);
+                  }
                 }
               }
-            }
 #pragma unroll
-            for (int t = 0; t < EPL; ++t)
-              if (cur[t] != 0u) cand_bits &= ~(1u << t);
+              for (int t = 0; t < EPL; ++t)
+                if (cur[t] != 0u) cand_bits &= ~(1u << t);
+            }
           }
           __syncwarp();
           // (4) compact candidates in gather order
@@ -582,6 +674,7 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           vis_n += nc;
           if (nc == 0) continue;
           dist_evals += nc;
+          prefetch_rows(a.X, a.dp, cp, nc);
           pad_cands(cp, nc);
           score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc);
           L = admit(qe, cd, cs, cp, rr, L, nc, sh.itopk, fu);
@@ -728,6 +821,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   int per_sm = 1;
   with_kernel(nc, epl, full, [&](auto kern) {
     GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
   });
   per_sm = std::max(per_sm, 1);
