@@ -198,12 +198,14 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
                                       const uint32_t* cp, double* cd, uint32_t n) {
   constexpr int G = GroupOf<NC>::G;
   const uint32_t lane = lane_id();
+  const char* xl = reinterpret_cast<const char*>(X + lane * 4);  // this lane's first column
+  const uint32_t rowb = dp * 4;
   __syncwarp();
   for (uint32_t base = 0; base < n; base += G) {
     float4 x[G][NC];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float* row = X + (uint64_t)cp[base + g] * dp + lane * 4;
+      const float* row = reinterpret_cast<const float*>(xl + (uint64_t)cp[base + g] * rowb);
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         if (FULL)
@@ -551,6 +553,8 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
       const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
       __syncwarp();
+      clear_words(dd, sh.dsz);  // (the seed stage used it) all-zero from here on
+      __syncwarp();
       uint32_t vis_n = ns;
       uint32_t fu = 0;  // every queue entry before fu is expanded
       if (ns > 0) {
@@ -589,7 +593,6 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           }
           iterations++;
           expanded += nf;
-          clear_words(dd, sh.dsz);
           // (1) adjacency entries of the frontier rows + their {scalar, slot}
           uint32_t v[EPL];
           uint2 at[EPL];
@@ -608,13 +611,40 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           // (2) drop SENTINEL / slot >= n, per-iteration unique, scalar pre-check
           uint32_t cand_bits = 0;
 #pragma unroll
-          for (int t = 0; t < EPL; ++t) {
-            const bool uq = set_insert_w(dd, dlg, v[t], at[t].y < a.n_live);
-            const float sv = __uint_as_float(at[t].x);
-            const bool inr = sv >= lo_f && sv <= hi_f;
-            gath_l += uq;
-            rej_l += uq && !inr;
-            cand_bits |= (uq && inr) ? 1u << t : 0u;
+          {
+            // every first-probe CAS in flight before any is consumed; the table
+            // (load <= 1/4) is left all-zero again by undoing this iteration's inserts
+            const uint32_t dmask = (1u << dlg) - 1;
+            uint32_t hs[EPL], dc[EPL], act = 0, pend = 0;
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) {
+              act |= at[t].y < a.n_live ? 1u << t : 0u;
+              hs[t] = hash32(v[t]) >> (32 - dlg);
+              dc[t] = ((act >> t) & 1u) ? atomicCAS(dd + hs[t], 0u, v[t] + 1) : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) pend |= (((act >> t) & 1u) && dc[t] != 0u && dc[t] != v[t] + 1) ? 1u << t : 0u;
+            while (__any_sync(kFull, pend != 0u)) {
+#pragma unroll
+              for (int t = 0; t < EPL; ++t) {
+                if ((pend >> t) & 1u) {
+                  hs[t] = (hs[t] + 1) & dmask;
+                  dc[t] = atomicCAS(dd + hs[t], 0u, v[t] + 1);
+                  if (dc[t] == 0u || dc[t] == v[t] + 1) pend &= ~(1u << t);
+                }
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) {
+              const bool uq = ((act >> t) & 1u) && dc[t] == 0u;
+              if (uq) dd[hs[t]] = 0u;
+              const float sv = __uint_as_float(at[t].x);
+              const bool inr = sv >= lo_f && sv <= hi_f;
+              gath_l += uq;
+              rej_l += uq && !inr;
+              cand_bits |= (uq && inr) ? 1u << t : 0u;
+            }
           }
           __syncwarp();
           // (3) exact visited set: every first-probe atomic of the iteration in flight at once
@@ -767,7 +797,7 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   s.width = width;
   const uint32_t fan = width * k_max;
   s.cmax = 1u << ceil_log2(std::max<uint64_t>(std::max(fan, want), 32));  // bitonic pads to a power of 2
-  s.dsz = 1u << ceil_log2(std::max<uint64_t>(2ull * fan, 128));
+  s.dsz = 1u << ceil_log2(std::max<uint64_t>(4ull * fan, 128));  // dedup table, load <= 1/4
   if (!worst) {
     s.vlog2 = std::min<uint32_t>(15, std::max<uint32_t>(11, ceil_log2((uint64_t)itopk * 24)));
   } else {
