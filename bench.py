@@ -45,28 +45,47 @@ def env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """Clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line), in-process through NVML (an nvidia-smi child per sample can stall
+    the GPU it is measuring); nvidia-smi is the fallback when NVML is missing."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period: float = 0.02):
         self.gpu = gpu
-        self.rows = []
+        self.period = period
+        self.rows = []  # (sm_mhz, sm_max_mhz, reasons-bitmask)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        except Exception:
+            self._nv = None
+
+    def _sample(self):
+        if self._nv is not None:
+            nv = self._nv
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.rows.append((float(sm), float(mx), int(rs)))
+            return
+        out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                              "clocks_event_reasons.active", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5)
+        for line in out.stdout.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            self.rows.append((float(f[0]), float(f[1]), int(f[2], 16)))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
+                self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t.start()
@@ -76,16 +95,16 @@ class ClockSampler:
         self._stop.set()
         self._t.join(timeout=6)
 
+    # NVML clocks-event-reason bits
+    BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
-                          and "Not" not in r[4 + i]})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for r in self.rows for bit, name in self.BITS.items() if r[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "via": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 def measured_peak_hbm():
@@ -291,6 +310,14 @@ def main():
     stats = np.frombuffer(res.stats.cpu().numpy().astype(np.uint32).tobytes(), dtype=_lib.STATS_DTYPE)
     bytes_q = algorithmic_bytes(stats, (dim + 3) // 4 * 4, 32, 10)
     achieved = bytes_q / (ms_step / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "search_traffic.json")) as f:
+            tr = json.load(f).get(f"{args.config}:itopk{itopk}:w{width}:it{iters}")
+        if tr and tr["queries"] == nq and n == PRESETS[args.config]["n"]:
+            traffic = tr["bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
 
     # ---- e2e through the public API with host buffers (H2D + D2H inside the region)
     Qh = np.ascontiguousarray(Q)
@@ -334,10 +361,12 @@ def main():
             "e2e": {"value": round(world * nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": None, "peak_kind": peak_kind,
+                         "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "k_search (filtered beam search)",
-                         "bytes_per_query": round(bytes_q / nq, 1)},
-            "gpu_launches": args.steps, "clocks": clk.summary(), "sweep": sweep}
+                         "algorithmic_bytes_per_launch": round(bytes_q), "bytes_per_query": round(bytes_q / nq, 1),
+                         "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/search_traffic.json)"},
+            # per step: the search grid + the (normally empty) overflow-retry grid
+            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "sweep": sweep}
     if cpu_idx is not None:
         procs = os.cpu_count() or 1
         idx = cpu_idx
