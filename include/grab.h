@@ -190,6 +190,24 @@ GRAB_API int grab_try_rewire(const float* X, uint64_t n_rows, uint32_t dim, uint
                     uint32_t v, uint32_t q, double sq_dvq, double alpha, uint32_t k_local,
                     int32_t* accepted, int32_t* evicted_pos);
 
+/* ---- bucket-range sharded search (no reference counterpart:
+ * the reference is single-process, so these replace nothing and follow the
+ * reference's result convention -- ascending (distance, slot) with GLOBAL slot
+ * ids, searcher.py:64-71). Device pointers, enqueued on `stream`. ----
+ * pack: per searched query q = qidx[i] (global query index), its k results
+ * (local slots -> gid[slot], -1 kept) go to send[(q / B) * B + q % B][0..k):
+ * the block of owner rank q / B. Every other block is filled NaN / -1. */
+GRAB_API int grab_shard_pack(uint64_t n, const uint32_t* qidx, const int64_t* slots, const double* dists,
+                             const int64_t* gid, uint32_t k, uint32_t world, uint32_t B, double* send_d,
+                             int64_t* send_i, void* stream);
+/* derive_query_seed(base, ordinals[i]) for a routed subset of a batch
+ * (searcher.py:85-87; host pointers) */
+GRAB_API int grab_derive_seeds(uint64_t base, const uint32_t* ordinals, uint64_t n, uint64_t* out);
+/* merge: recv[src][B][k] (after the all-to-all) -> per owned query the top-k of
+ * the nsrc lists by (distance, global id); out_c = result length. */
+GRAB_API int grab_merge_topk(uint32_t nq, uint32_t nsrc, uint32_t B, uint32_t k, const double* d,
+                             const int64_t* id, double* out_d, int64_t* out_i, uint32_t* out_c, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

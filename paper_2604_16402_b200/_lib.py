@@ -92,6 +92,9 @@ _SIGS = {
     "grab_read": (C.c_int, [P, C.c_int, u64, u64, P]),
     "grab_select_neighbors": (C.c_int, [P, u64, u32, i64, P, P, P, u32, u32, dbl, P, P]),
     "grab_try_rewire": (C.c_int, [P, u64, u32, P, u32, u32, u32, dbl, dbl, u32, P, P]),
+    "grab_shard_pack": (C.c_int, [u64, P, P, P, P, u32, u32, u32, P, P, P]),
+    "grab_merge_topk": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, P]),
+    "grab_derive_seeds": (C.c_int, [u64, P, u64, P]),
 }
 
 

@@ -12,6 +12,9 @@ namespace grab {
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // reference layout.py:19
 constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 
+// Records the thread-local message for grab_last_error() and returns `code`.
+int grab_set_error(int code, const char* msg);
+
 // Error carrying one of the GRAB_ERR_* codes; converted at the C-ABI edge.
 struct Error : std::runtime_error {
   int code;

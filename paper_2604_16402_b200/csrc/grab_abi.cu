@@ -24,6 +24,14 @@ static thread_local std::string g_err;
 
 extern "C" const char* grab_last_error(void) { return g_err.c_str(); }
 
+namespace grab {
+// for entry points defined in other translation units (shard.cu)
+int grab_set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace grab
+
 template <class F>
 static int guarded(F&& f) {
   try {
@@ -553,5 +561,11 @@ extern "C" int grab_sq_distances(const float* q, const float* rows, uint64_t n, 
     run_sq_distances(dq.as<float>(), dr.as<float>(), n, dp, dout.as<double>(), st);
     GRAB_CUDA(cudaMemcpyAsync(out, dout.p, n * 8, cudaMemcpyDeviceToHost, st));
     GRAB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" int grab_derive_seeds(uint64_t base, const uint32_t* ordinals, uint64_t n, uint64_t* out) {
+  return guarded([&] {
+    for (uint64_t i = 0; i < n; ++i) out[i] = derive_query_seed(base, ordinals[i]);
   });
 }

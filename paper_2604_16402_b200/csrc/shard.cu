@@ -1,0 +1,110 @@
+// Bucket-range sharded search: result packing and per-query top-k merge.
+//
+// The reference has no sharding (one process); this is the B200
+// design for indexes split across GPUs by contiguous scalar (= bucket) range
+// (SURVEY §8(e)): every rank searches only the queries whose range overlaps
+// its shard, packs its per-query top-k -- mapped to GLOBAL slot ids -- into
+// the block of the rank that owns the query, the blocks are exchanged with
+// one fixed-size all-to-all (NCCL over NVLink), and each owner merges the
+// world x k candidates of its queries by (distance, global slot), the
+// reference's tie rule (searcher.py:64-71).
+#include "index.cuh"
+
+namespace grab {
+
+// send[(owner * B + q % B) * k + j] for every searched query q = qidx[i];
+// blocks of unsearched queries keep the caller's 0xFF fill (NaN, -1).
+__global__ void k_shard_pack(uint64_t n, const uint32_t* __restrict__ qidx, const int64_t* __restrict__ slots,
+                             const double* __restrict__ dists, const int64_t* __restrict__ gid, uint32_t k,
+                             uint32_t B, double* __restrict__ send_d, int64_t* __restrict__ send_i) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= n * k) return;
+  const uint64_t i = t / k, j = t % k;
+  const uint32_t q = qidx[i];
+  const uint64_t dst = ((uint64_t)(q / B) * B + q % B) * k + j;
+  const int64_t s = slots[i * k + j];
+  send_d[dst] = s >= 0 ? dists[i * k + j] : __longlong_as_double(0x7FF8000000000000ll);
+  send_i[dst] = s >= 0 ? gid[s] : -1;
+}
+
+// One thread per owned query: k-way merge of nsrc ascending lists of k
+// (entries with id < 0 are empty) into the top-k by (distance, global id).
+__global__ void k_merge_topk(uint32_t nq, uint32_t nsrc, uint32_t B, uint32_t k, const double* __restrict__ d,
+                             const int64_t* __restrict__ id, double* __restrict__ out_d, int64_t* __restrict__ out_i,
+                             uint32_t* __restrict__ out_c) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  constexpr uint32_t kMaxSrc = 64;
+  uint32_t head[kMaxSrc];
+  for (uint32_t r = 0; r < nsrc; ++r) head[r] = 0;
+  uint32_t c = 0;
+  while (c < k) {
+    int best = -1;
+    double bd = 0;
+    int64_t bi = 0;
+    for (uint32_t r = 0; r < nsrc; ++r) {
+      if (head[r] >= k) continue;
+      const uint64_t o = ((uint64_t)r * B + q) * k + head[r];
+      const int64_t ii = id[o];
+      if (ii < 0) {
+        head[r] = k;  // lists are dense prefixes
+        continue;
+      }
+      const double dd = d[o];
+      if (best < 0 || dd < bd || (dd == bd && ii < bi)) {
+        best = (int)r;
+        bd = dd;
+        bi = ii;
+      }
+    }
+    if (best < 0) break;
+    out_d[(uint64_t)q * k + c] = bd;
+    out_i[(uint64_t)q * k + c] = bi;
+    head[best]++;
+    ++c;
+  }
+  for (uint32_t j = c; j < k; ++j) {
+    out_d[(uint64_t)q * k + j] = __longlong_as_double(0x7FF8000000000000ll);
+    out_i[(uint64_t)q * k + j] = -1;
+  }
+  out_c[q] = c;
+}
+
+}  // namespace grab
+
+using namespace grab;
+
+extern "C" GRAB_API int grab_shard_pack(uint64_t n, const uint32_t* qidx, const int64_t* slots, const double* dists,
+                                        const int64_t* gid, uint32_t k, uint32_t world, uint32_t B, double* send_d,
+                                        int64_t* send_i, void* stream) {
+  try {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (k == 0 || world == 0 || B == 0) throw Error(GRAB_ERR_VALUE, "k, world and B must be >= 1");
+    GRAB_CUDA(cudaMemsetAsync(send_d, 0xFF, (size_t)world * B * k * sizeof(double), st));
+    GRAB_CUDA(cudaMemsetAsync(send_i, 0xFF, (size_t)world * B * k * sizeof(int64_t), st));
+    if (n) {
+      k_shard_pack<<<(unsigned)div_up(n * k, 256), 256, 0, st>>>(n, qidx, slots, dists, gid, k, B, send_d, send_i);
+      GRAB_CHECK_LAUNCH();
+    }
+    return GRAB_OK;
+  } catch (const Error& e) {
+    return grab_set_error(e.code, e.what());
+  }
+}
+
+extern "C" GRAB_API int grab_merge_topk(uint32_t nq, uint32_t nsrc, uint32_t B, uint32_t k, const double* d,
+                                        const int64_t* id, double* out_d, int64_t* out_i, uint32_t* out_c,
+                                        void* stream) {
+  try {
+    if (nsrc > 64) throw Error(GRAB_ERR_VALUE, "at most 64 shards");
+    if (nq > B) throw Error(GRAB_ERR_VALUE, "owned queries exceed the block size");
+    if (nq) {
+      k_merge_topk<<<(unsigned)div_up(nq, 128), 128, 0, (cudaStream_t)stream>>>(nq, nsrc, B, k, d, id, out_d, out_i,
+                                                                                out_c);
+      GRAB_CHECK_LAUNCH();
+    }
+    return GRAB_OK;
+  } catch (const Error& e) {
+    return grab_set_error(e.code, e.what());
+  }
+}

@@ -1,0 +1,131 @@
+"""Multi-process driver for the sharded-index tests (run as a script by
+tests/test_shard.py): spawns `world` ranks on 127.0.0.1 with the gloo backend.
+
+  --mode exchange   CPU only: plan / route / pack-layout / all-to-all / merge
+                    semantics checked against the numpy restatements.
+  --mode gpu        every rank shares cuda:0: builds its shard with libgrab,
+                    serves a query batch through route -> search -> pack ->
+                    all-to-all -> merge, and rank 0 checks the merged exact
+                    pipeline against the single-index brute force (bit-exact
+                    ids) and the search recall against it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def _init(rank, world, port):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def run_exchange(rank, world, port, out):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_16402_b200 import shard as sh
+
+    _init(rank, world, port)
+    k, nq = 5, 13
+    B = sh.owner_block(nq, world)
+    g = np.random.default_rng(100 + rank)
+    # this rank's local top-k lists for the queries it "searched" (ascending)
+    mine = np.sort(g.choice(nq, size=nq // 2 + rank, replace=False)).astype(np.int64)
+    d = np.sort(g.random((len(mine), k)), axis=1)
+    ids = (rank * 1000 + g.integers(0, 1000, size=(len(mine), k))).astype(np.int64)
+    ids[:, -1] = np.where(np.arange(len(mine)) % 3 == 0, -1, ids[:, -1])  # some short lists
+    d[ids < 0] = np.nan
+    send_d = np.full((world, B, k), np.nan)
+    send_i = np.full((world, B, k), -1, dtype=np.int64)
+    for row, q in enumerate(mine):  # restated grab_shard_pack layout
+        send_d[q // B, q % B] = d[row]
+        send_i[q // B, q % B] = ids[row]
+    rd, ri = sh.exchange(torch.from_numpy(send_d), torch.from_numpy(send_i), world)
+    # gather every rank's raw lists to check the merge against a global sort
+    alld = [torch.empty((world, B, k), dtype=torch.float64) for _ in range(world)]
+    alli = [torch.empty((world, B, k), dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(alld, torch.from_numpy(send_d))
+    dist.all_gather(alli, torch.from_numpy(send_i))
+    n_own = max(0, min(B, nq - rank * B))
+    ms, md, mc = sh.merge_reference(rd.numpy(), ri.numpy(), n_own, k)
+    ok = True
+    for j in range(n_own):
+        q = rank * B + j
+        cand = sorted((float(alld[r][rank, j, c]), int(alli[r][rank, j, c])) for r in range(world)
+                      for c in range(k) if int(alli[r][rank, j, c]) >= 0)[:k]
+        ok &= [i for _, i in cand] == ms[j, : mc[j]].tolist()
+        ok &= q // B == rank
+    res = torch.tensor([1 if ok else 0])
+    dist.all_reduce(res)
+    if rank == 0:
+        with open(out, "w") as f:
+            json.dump({"ok": int(res.item()) == world}, f)
+    dist.destroy_process_group()
+
+
+def run_gpu(rank, world, port, out):
+    import numpy as np
+    import torch
+
+    import paper_2604_16402_b200 as g
+    from paper_2604_16402_b200 import datasets as ds
+    from paper_2604_16402_b200 import shard as sh
+
+    _init(rank, world, port)
+    torch.cuda.set_device(0)
+    n, d, nq, k = 12_000, 32, 200, 10
+    X, S = ds.gen_lowrank(n, d, seed=0)
+    Q = ds.lowrank_queries(nq, d, seed=1)
+    lo, hi = ds.range_arrays(ds.generate_ranges(S, 0.2, nq, 0))
+    cuts = sh.plan_shards(S, world)
+    owner = sh.shard_of(S, cuts)
+    gid = np.nonzero(owner == rank)[0]
+    params = g.BuildParams(k_max=16, k_local=8, bucket_capacity=500)
+    idx, _ = sh.ShardedIndex.build(X[gid], S[gid], gid, params, rank=rank, world=world, device=0)
+    sp = g.SearchParams(k=k, itopk=64)
+    ex = idx.search(Q, lo, hi, sp, exact=True)
+    se = idx.search(Q, lo, hi, sp, seed_base=0)
+    torch.cuda.synchronize()
+    import torch.distributed as dist
+    parts = []
+    for t in (ex.slots, ex.counts, se.slots, se.counts):
+        tc = t.cpu()
+        B = sh.owner_block(nq, world)
+        pad = torch.full((B,) + tuple(tc.shape[1:]), -1, dtype=tc.dtype)
+        pad[: tc.shape[0]] = tc
+        lst = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(lst, pad)
+        parts.append(torch.cat(lst)[:nq].numpy())
+    if rank == 0:
+        gi, _ = g.build_index(X, S, params)  # the single index over all rows
+        ts, td, tcnt = g.brute_force_arrays(gi, Q, lo, hi, k)
+        exact_ok = all(parts[0][i, : parts[1][i]].tolist() == ts[i, : tcnt[i]].tolist() for i in range(nq))
+        rec = ds.batch_recall(parts[2], parts[3], ts, tcnt, k)
+        with open(out, "w") as f:
+            json.dump({"exact_ok": bool(exact_ok), "recall": rec, "routed": int(se.routed)}, f)
+    dist.destroy_process_group()
+
+
+def main():
+    import torch.multiprocessing as mp
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", choices=["exchange", "gpu"], required=True)
+    ap.add_argument("--world", type=int, default=2)
+    ap.add_argument("--port", type=int, default=29533)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    fn = run_exchange if a.mode == "exchange" else run_gpu
+    mp.spawn(fn, args=(a.world, a.port, a.out), nprocs=a.world)
+
+
+if __name__ == "__main__":
+    main()
