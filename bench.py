@@ -34,7 +34,8 @@ PRESETS = {
     "cfg3": dict(n=1_000_000, dim=960, cap=10_000, nq=10_000, sel=0.10),
 }
 GRID = [(32, 1, 50), (32, 2, 50), (48, 2, 50), (64, 2, 50), (64, 4, 50), (96, 4, 50), (128, 4, 50), (192, 4, 50),
-        (128, 4, 100), (160, 4, 100), (192, 4, 100), (224, 4, 100), (256, 4, 100), (192, 2, 100), (256, 2, 150)]
+        (128, 4, 100), (160, 4, 100), (192, 4, 100), (224, 4, 100), (256, 4, 100), (192, 2, 100), (256, 2, 150),
+        (288, 4, 100), (304, 4, 100), (320, 4, 100), (352, 4, 120), (384, 4, 120), (448, 4, 150)]
 
 
 def env_int(k, d):
@@ -194,6 +195,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--insert-batch", type=int, default=100_000)
+    ap.add_argument("--global-pass", default="auto", choices=["auto", "exact", "descent"],
+                    help="pass-2 graph: auto = the reference rule (NN-descent above 100K rows)")
     args = ap.parse_args()
     cfg = dict(PRESETS[args.config])
     for key in ("n", "dim", "cap", "nq", "sel"):
@@ -226,7 +229,7 @@ def main():
     # ---- build (replicated per rank; deterministic)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    gi, brep = g.build_index(X, S, params, device=local)
+    gi, brep = g.build_index(X, S, params, device=local, global_pass=args.global_pass)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
 
@@ -263,7 +266,8 @@ def main():
               "n": n, "dim": dim, "bucket_capacity": cap, "m": brep.m, "queries_per_gpu": nq, "selectivity": sel,
               "k": 10, "itopk": itopk, "search_width": width, "max_iterations": iters, "recall_at_10": recall,
               "k_max": 32, "k_local": 16, "l2": f"inputs larger than L2 (X = {n * dim * 4 / 1e6:.0f} MB > 126 MB)",
-              "index": "replicated per GPU" if world > 1 else "single GPU"}
+              "index": "replicated per GPU" if world > 1 else "single GPU",
+              "global_pass": brep.global_pass}
 
     if args.impl == "reference":
         procs = os.cpu_count() or 1

@@ -53,8 +53,13 @@ extern "C" {
 typedef struct grab_index grab_index;
 
 /* BuildParams (core.py:85-118) */
+/* global_pass: pass-2 candidate graph (builder.py:379-391) */
+#define GRAB_GLOBAL_AUTO 0    /* reference rule: exact kNN iff n <= 100 000, else NN-descent */
+#define GRAB_GLOBAL_EXACT 1   /* exact kNN at every n (tcgen05 screen + f64 rerank) */
+#define GRAB_GLOBAL_DESCENT 2 /* random init + refine_rounds of neighborhood descent */
+
 typedef struct {
-  uint32_t k_max, k_local, bucket_capacity, _pad;
+  uint32_t k_max, k_local, bucket_capacity, global_pass;
   double proximal_fraction, proximal_window, alpha;
   uint64_t rng_seed;
 } grab_build_params;
@@ -76,6 +81,7 @@ typedef struct {
   uint32_t m, isolated_nodes;
   double phase1_seconds, phase2_seconds, fuse_seconds, total_seconds;
   double cross_bucket_edge_ratio;
+  uint32_t global_descent, _pad; /* 1 when pass 2 ran NN-descent */
 } grab_build_report;
 
 /* InsertReport (updater.py:31-46); rewired rows via grab_last_rewired() */

@@ -28,7 +28,7 @@ class GrabDeviceError(RuntimeError):
 
 class BuildParamsC(C.Structure):
     _fields_ = [("k_max", C.c_uint32), ("k_local", C.c_uint32), ("bucket_capacity", C.c_uint32),
-                ("_pad", C.c_uint32), ("proximal_fraction", C.c_double), ("proximal_window", C.c_double),
+                ("global_pass", C.c_uint32), ("proximal_fraction", C.c_double), ("proximal_window", C.c_double),
                 ("alpha", C.c_double), ("rng_seed", C.c_uint64)]
 
 
@@ -45,7 +45,8 @@ STATS_DTYPE = np.dtype([(f, "<u4") for f in STAT_FIELDS])
 class BuildReportC(C.Structure):
     _fields_ = [("n", C.c_uint64), ("m", C.c_uint32), ("isolated_nodes", C.c_uint32),
                 ("phase1_seconds", C.c_double), ("phase2_seconds", C.c_double), ("fuse_seconds", C.c_double),
-                ("total_seconds", C.c_double), ("cross_bucket_edge_ratio", C.c_double)]
+                ("total_seconds", C.c_double), ("cross_bucket_edge_ratio", C.c_double),
+                ("global_descent", C.c_uint32), ("_pad", C.c_uint32)]
 
 
 INSERT_FIELDS = ["batch_size", "bulk_built", "forward_accepted", "forward_rejected", "reverse_accepted",

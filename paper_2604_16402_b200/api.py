@@ -262,6 +262,7 @@ class BuildReport:
     bucket_sizes: list = field(default_factory=list)
     isolated_nodes: int = 0
     cross_bucket_edge_ratio: float = 0.0
+    global_pass: str = "exact"  # (ours) what pass 2 ran: "exact" kNN or "descent"
 
     def to_dict(self) -> dict:
         return dict(self.__dict__)
@@ -282,8 +283,12 @@ _STRATEGY = {"quantile": 0, "width": 1}
 
 def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None = None, headroom: float = 2.0,
                 bucket_strategy: str = "quantile", n_threads: int = 1, k_g: int | None = None,
-                refine_rounds: int = 3, device: int = 0, return_draft: bool = False):
+                refine_rounds: int = 3, device: int = 0, return_draft: bool = False, global_pass: str = "auto"):
     """Full static build on the device: partition, slab layout, pass 1, pass 2, fuse, repair.
+
+    ``global_pass`` (ours): "auto" follows the reference (exact global kNN for
+    n <= 100 000, random init + ``refine_rounds`` NN-descent rounds above);
+    "exact" / "descent" force one.
 
     Returns (GraphIndex, BuildReport) like the reference, plus a BuildDraft when
     ``return_draft``. ``n_threads`` is accepted for signature parity (the GPU is
@@ -313,7 +318,7 @@ def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None =
         mem = L.MEM_HOST
     if capacity is None:
         capacity = max(int(n * headroom), n)
-    index = create_index(dim, capacity, params, device)
+    index = create_index(dim, capacity, params, device, global_pass)
     kg = params.k_max if k_g is None else int(k_g)
     rep = L.BuildReportC()
     dbg = None
@@ -333,7 +338,8 @@ def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None =
                          total_seconds=rep.total_seconds,
                          bucket_sizes=[len(b) for b in meta.bucket_to_index] if meta else [],
                          isolated_nodes=int(rep.isolated_nodes),
-                         cross_bucket_edge_ratio=float(rep.cross_bucket_edge_ratio))
+                         cross_bucket_edge_ratio=float(rep.cross_bucket_edge_ratio),
+                         global_pass="descent" if rep.global_descent else "exact")
     if return_draft:
         return index, report, draft
     return index, report

@@ -574,9 +574,13 @@ uint32_t reinforce_device(DevIndex& ix, const uint32_t* rows, uint64_t n, cudaSt
   return total;
 }
 
+constexpr uint64_t kExactGlobalLimit = 100000;  // EXACT_GLOBAL_LIMIT, builder.py:33
+constexpr uint32_t kDescentSample = 8;            // descent_sample, builder.py:369
+void descent_device(const DevIndex& ix, uint64_t n, uint32_t k, uint32_t rounds, uint32_t sample, uint32_t* gf,
+                    double* gd, cudaStream_t st);  // descent.cu
+
 void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_rounds, grab_build_report* rep,
                         const grab_build_debug* dbg, cudaStream_t st) {
-  (void)refine_rounds;  // exact global kNN at every scale
   const uint32_t K = ix.params.k_max;
   Scratch S(st);
   uint32_t* rows = S.alloc<uint32_t>(n);  // phys rows in slot order
@@ -660,10 +664,19 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
     uint32_t* gf = S.alloc<uint32_t>(ix.phys_cap * (uint64_t)k_g);
     double* gd = S.alloc<double>(ix.phys_cap * (uint64_t)k_g);
     GRAB_CUDA(cudaMemsetAsync(gf, 0xFF, ix.phys_cap * (uint64_t)k_g * 4, st));
-    std::vector<KnnJob> jobs;
-    const uint32_t pend = ix.h_bstart.back() + ix.h_bcount.back();
-    for (uint32_t r = 0; r < pend; r += kKnnBM) jobs.push_back({r, std::min<uint32_t>(kKnnBM, pend - r), 0, pend});
-    knn_device(ix, norms, jobs, k_g, /*tiebreak slot=*/true, gf, gd, st);
+    // build_global_graph (builder.py:379-391): exact kNN at n <= EXACT_GLOBAL_LIMIT,
+    // random init + neighborhood descent above (global_pass overrides)
+    const uint32_t gp = ix.params.global_pass;
+    const bool descent = gp == GRAB_GLOBAL_DESCENT || (gp == GRAB_GLOBAL_AUTO && n > kExactGlobalLimit);
+    rep->global_descent = descent ? 1 : 0;
+    if (descent) {
+      descent_device(ix, n, k_g, refine_rounds, kDescentSample, gf, gd, st);
+    } else {
+      std::vector<KnnJob> jobs;
+      const uint32_t pend = ix.h_bstart.back() + ix.h_bcount.back();
+      for (uint32_t r = 0; r < pend; r += kKnnBM) jobs.push_back({r, std::min<uint32_t>(kKnnBM, pend - r), 0, pend});
+      knn_device(ix, norms, jobs, k_g, /*tiebreak slot=*/true, gf, gd, st);
+    }
     uint32_t* cnt = S.alloc<uint32_t>(ix.phys_cap + 1);
     uint32_t* off = S.alloc<uint32_t>(ix.phys_cap + 1);
     uint32_t* fill = S.alloc<uint32_t>(ix.phys_cap);

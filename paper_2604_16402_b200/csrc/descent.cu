@@ -1,0 +1,522 @@
+// Pass-2 global graph above the exact limit: random init + neighborhood
+// descent (reference builder.py:288-335, 364-393), on the device.
+//
+// Restated semantics (slot space, n nodes, k = k_g, s = descent_sample):
+//   init    rng = default_rng([rng_seed, 1]);
+//           graph = rng.integers(0, n - 1, size=(n, k)); graph[graph >= row] += 1
+//           (numpy's bounded fill: Lemire 32-bit draws over a fill-local buffer
+//           of the PCG64 stream, low half first) -- regenerated bit-exactly here
+//           with 128-bit LCG jump-ahead, an accept scan and a scatter.
+//   round   joint = [graph | reverse_topk(graph, dists, k)] (2k columns, the
+//           reverse part = nearest k sources by (dist, src));
+//           hop = rng.permutation(2k)[:2s] (numpy shuffle, bitgen-level 32-bit
+//           buffer -- restated on the host);
+//           candidates of v = joint[v] ++ joint[joint[v][h]] for h in hop (-1 if
+//           missing); distance inf for missing, self and every repeat of an id
+//           (first occurrence kept); new row = top-k by (dist, column).
+// Distances are f64-accumulated then rounded to f32 (the reference's einsum
+// accumulates in f32; values agree to the last bits, ids up to near-ties).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "index.cuh"
+#include "rng.cuh"
+
+namespace grab {
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st);  // build.cu
+
+namespace {
+
+struct ScratchD {
+  std::vector<void*> ptrs;
+  cudaStream_t st;
+  explicit ScratchD(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    GRAB_CUDA(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  ~ScratchD() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+// (A, G) of a jump by m steps: s_m = A s + G inc.
+struct Jump {
+  u128 a, g;
+};
+
+__host__ __device__ inline Jump jump_compose(const Jump& x, const Jump& y) {  // x then y
+  return Jump{y.a * x.a, y.a * x.g + y.g};
+}
+
+struct JumpPow2 {
+  u128 a[64], g[64];
+};
+
+JumpPow2 make_pow2() {
+  JumpPow2 t;
+  Jump j{pcg_mult(), 1};
+  for (int b = 0; b < 64; ++b) {
+    t.a[b] = j.a;
+    t.g[b] = j.g;
+    j = jump_compose(j, j);
+  }
+  return t;
+}
+
+__host__ __device__ inline Jump jump_by(const u128* pa, const u128* pg, uint64_t m) {
+  Jump acc{1, 0};
+  for (int b = 0; m; ++b, m >>= 1)
+    if (m & 1) acc = jump_compose(acc, Jump{pa[b], pg[b]});
+  return acc;
+}
+
+// Host PCG64 with numpy's bitgen-level 32-bit buffer (pcg64_next32).
+struct HostPcg {
+  u128 state, inc;
+  bool has32 = false;
+  uint32_t buf32 = 0;
+  uint64_t next64() {
+    state = state * pcg_mult() + inc;
+    return pcg_xsl_rr(state);
+  }
+  uint32_t next32() {
+    if (has32) {
+      has32 = false;
+      return buf32;
+    }
+    const uint64_t x = next64();
+    has32 = true;
+    buf32 = (uint32_t)(x >> 32);
+    return (uint32_t)x;
+  }
+  // random_interval(max): masked rejection over next32 (max < 2^32)
+  uint32_t interval(uint32_t mx) {
+    if (mx == 0) return 0;
+    uint32_t mask = mx;
+    mask |= mask >> 1;
+    mask |= mask >> 2;
+    mask |= mask >> 4;
+    mask |= mask >> 8;
+    mask |= mask >> 16;
+    uint32_t v;
+    while ((v = (next32() & mask)) > mx) {
+    }
+    return v;
+  }
+  // Generator.permutation(n): arange + Fisher-Yates from the top
+  std::vector<uint32_t> permutation(uint32_t n) {
+    std::vector<uint32_t> a(n);
+    for (uint32_t i = 0; i < n; ++i) a[i] = i;
+    for (uint32_t i = n - 1; i >= 1; --i) std::swap(a[i], a[interval(i)]);
+    return a;
+  }
+};
+
+// default_rng([a, b]) state (SeedSequence over two words)
+Pcg64 pcg64_from_pair(uint64_t a, uint64_t b) {
+  uint64_t e[2] = {a, b};
+  SeedSeq s = seedseq_from_u64s(e, 2);
+  uint64_t v[4];
+  seedseq_u64(s, v, 4);
+  const u128 initstate = ((u128)v[0] << 64) | v[1];
+  const u128 initseq = ((u128)v[2] << 64) | v[3];
+  Pcg64 g;
+  g.inc = (initseq << 1) | 1;
+  g.state = g.inc;
+  g.state += initstate;
+  g.state = g.state * pcg_mult() + g.inc;
+  return g;
+}
+
+constexpr uint32_t kOutPerThread = 64;  // PCG outputs (128 words) per thread
+
+// Word i of the stream (low/high halves of output i/2): Lemire accept flag and value.
+__global__ void k_init_words(u128 s0, u128 inc, const u128* pa, const u128* pg, uint64_t n_out, uint32_t total,
+                             uint32_t thresh, uint32_t* flag, uint32_t* val) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t o0 = t * kOutPerThread;
+  if (o0 >= n_out) return;
+  const Jump j = jump_by(pa, pg, o0);
+  u128 s = j.a * s0 + j.g * inc;
+  const uint64_t o1 = o0 + kOutPerThread < n_out ? o0 + kOutPerThread : n_out;
+  for (uint64_t o = o0; o < o1; ++o) {
+    s = s * pcg_mult() + inc;
+    const uint64_t x = pcg_xsl_rr(s);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t w = (uint32_t)(x >> (32 * h));
+      const uint64_t m = (uint64_t)w * total;
+      flag[2 * o + h] = (uint32_t)m >= thresh ? 1u : 0u;
+      val[2 * o + h] = (uint32_t)(m >> 32);
+    }
+  }
+}
+
+// graph[d] = value of the d-th accepted word (+1 when >= its row: no self)
+__global__ void k_init_scatter(uint64_t n_words, const uint32_t* flag, const uint32_t* pos, const uint32_t* val,
+                               uint64_t nk, uint32_t k, int32_t* graph, unsigned long long* last_word) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n_words || !flag[i]) return;
+  const uint64_t d = pos[i];
+  if (d >= nk) return;
+  const uint32_t row = (uint32_t)(d / k);
+  uint32_t v = val[i];
+  if (v >= row) v += 1;
+  graph[d] = (int32_t)v;
+  if (d == nk - 1) *last_word = i;
+}
+
+// f64-accumulated squared distance between slot rows a and b, rounded to f32;
+// 8 lanes per pair (lane group g = lane / 8), dp/4 float4 per row.
+__device__ __forceinline__ float group_dist(const float* X, uint32_t dp, uint32_t pa, uint32_t pb, uint32_t sub,
+                                            bool active) {
+  double acc = 0.0;
+  if (active) {
+    const float* ra = X + (uint64_t)pa * dp;
+    const float* rb = X + (uint64_t)pb * dp;
+    for (uint32_t f = sub; f * 4 < dp; f += 8) {
+      const float4 x = ldg_nc_f4(rb + 4 * f);
+      const float4 q = *reinterpret_cast<const float4*>(ra + 4 * f);
+      acc = sq4(x, q, acc);
+    }
+  }
+  acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 4);
+  acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 2);
+  acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 1);
+  return active ? (float)acc : __int_as_float(0x7F800000);
+}
+
+// init distances: one 8-lane group per edge
+__global__ void k_edge_dists(const int32_t* graph, uint64_t nk, uint32_t k, const uint32_t* s2p, const float* X,
+                             uint32_t dp, float* dist) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  const uint64_t e = w * 4 + lane / 8;
+  const bool ok = e < nk && graph[e < nk ? e : 0] >= 0;
+  const uint32_t row = (uint32_t)(e / k);
+  const float d = group_dist(X, dp, ok ? s2p[row] : 0, ok ? s2p[graph[e]] : 0, lane & 7, ok);
+  if (e < nk && (lane & 7) == 0) dist[e] = d;
+}
+
+// reverse top-k: key2 = (dist bits << 32 | src), sorted stably by dst afterwards
+__global__ void k_rev_keys(const int32_t* graph, const float* dist, uint64_t nk, uint32_t k, uint32_t n,
+                           uint64_t* key2, uint32_t* dst) {
+  const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (e >= nk) return;
+  const int32_t v = graph[e];
+  key2[e] = ((uint64_t)__float_as_uint(dist[e]) << 32) | (uint32_t)(e / k);
+  dst[e] = v >= 0 ? (uint32_t)v : n;  // missing edges sort past every node
+}
+
+__global__ void k_count_dst(const uint32_t* dst, uint64_t nk, uint32_t n, uint32_t* cnt) {
+  const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (e < nk && dst[e] < n) atomicAdd(cnt + dst[e], 1u);
+}
+
+// joint[v] = [graph[v] (k) | nearest k reverse sources (-1 padded)]
+__global__ void k_joint(const int32_t* graph, uint32_t n, uint32_t k, const uint32_t* sdst, const uint64_t* skey,
+                        const uint32_t* off, uint64_t nk, int32_t* joint) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < (uint64_t)n * k) {
+    const uint64_t v = i / k, j = i % k;
+    joint[v * 2 * k + j] = graph[i];
+    joint[v * 2 * k + k + j] = -1;
+  }
+}
+
+__global__ void k_joint_rev(uint32_t n, uint32_t k, const uint32_t* sdst, const uint64_t* skey, const uint32_t* off,
+                            uint64_t nk, int32_t* joint) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= nk) return;
+  const uint32_t v = sdst[i];
+  if (v >= n) return;
+  const uint64_t pos = i - off[v];
+  if (pos < k) joint[(uint64_t)v * 2 * k + k + pos] = (int32_t)(uint32_t)skey[i];
+}
+
+// Key of a (dist, column) candidate as one u64: f32 bits above the column.
+__device__ __forceinline__ uint64_t dc_key(float d, uint32_t col) {
+  return ((uint64_t)__float_as_uint(d) << 32) | col;
+}
+
+// One descent round: one warp per node. Shared memory per warp: candidate ids
+// [C], their dedup slot [C] (u16), f32 distances [C], and a 2H-entry id hash
+// (keys) with the minimum column per key.
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint32_t n, uint32_t k,
+                                                      const uint32_t* hop, uint32_t nhop, const uint32_t* s2p,
+                                                      const float* X, uint32_t dp, uint32_t C, uint32_t H,
+                                                      int32_t* out_graph, float* out_dist) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t v = blockIdx.x * WPB + wib;
+  if (v >= n) return;  // warp-uniform
+  uint8_t* base = smem + (size_t)wib * (C * 10 + H * 8);
+  int32_t* cid = (int32_t*)base;
+  float* cd = (float*)(base + C * 4);
+  uint32_t* hkey = (uint32_t*)(base + C * 8);
+  uint32_t* hcol = hkey + H;
+  uint16_t* cslot = (uint16_t*)(hcol + H);
+  const uint32_t J = 2 * k;
+  const int32_t* jv = joint + (uint64_t)v * J;
+  // (a) candidate ids: own joint row, then the joint rows of the hop sources
+  for (uint32_t i = lane; i < H; i += 32) {
+    hkey[i] = 0;
+    hcol[i] = 0xFFFFFFFFu;
+  }
+  for (uint32_t i = lane; i < J; i += 32) cid[i] = jv[i];
+  for (uint32_t h = 0; h < nhop; ++h) {
+    const int32_t src = jv[hop[h]];
+    for (uint32_t i = lane; i < J; i += 32) cid[J + h * J + i] = src >= 0 ? joint[(uint64_t)src * J + i] : -1;
+  }
+  __syncwarp();
+  // (b) first occurrence per id: hash id -> min column (warp-uniform probing)
+  const uint32_t hmask = H - 1;
+  for (uint32_t b0 = 0; b0 < C; b0 += 32) {
+    const uint32_t c = b0 + lane;
+    const int32_t id = c < C ? cid[c] : -1;
+    bool act = id >= 0;
+    uint32_t h = ((uint32_t)id * 0x9E3779B1u) & hmask;
+    uint32_t cur = act ? atomicCAS(hkey + h, 0u, (uint32_t)id + 1) : 0u;
+    bool pend = act && cur != 0u && cur != (uint32_t)id + 1;
+    while (__any_sync(0xFFFFFFFFu, pend)) {
+      if (pend) {
+        h = (h + 1) & hmask;
+        cur = atomicCAS(hkey + h, 0u, (uint32_t)id + 1);
+        pend = cur != 0u && cur != (uint32_t)id + 1;
+      }
+    }
+    if (act) atomicMin(hcol + h, c);
+    if (c < C) cslot[c] = act ? (uint16_t)h : (uint16_t)0xFFFF;
+  }
+  __syncwarp();
+  // (c) distances (inf: missing, self, repeat): 8-lane groups, 4 candidates
+  // per group per step (16 rows in flight per warp)
+  const uint32_t pv = s2p[v];
+  const float* qrow = X + (uint64_t)pv * dp;
+  const uint32_t sub = lane & 7, grp = lane >> 3;
+  for (uint32_t b0 = 0; b0 < C; b0 += 16) {
+    uint32_t pc[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t c = b0 + grp * 4 + u;
+      ok[u] = false;
+      pc[u] = 0;
+      if (c < C) {
+        const int32_t id = cid[c];
+        ok[u] = id >= 0 && (uint32_t)id != v && hcol[cslot[c]] == c;
+        if (ok[u]) pc[u] = s2p[id];
+      }
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+    for (uint32_t f = sub; f * 4 < dp; f += 8) {
+      const float4 q = *reinterpret_cast<const float4*>(qrow + 4 * f);
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = ok[u] ? ldg_nc_f4(X + (uint64_t)pc[u] * dp + 4 * f) : q;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = sq4(x[u], q, acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 4);
+      acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 2);
+      acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 1);
+      const uint32_t c = b0 + grp * 4 + u;
+      if (c < C && sub == 0) cd[c] = ok[u] ? (float)acc[u] : __int_as_float(0x7F800000);
+    }
+  }
+  __syncwarp();
+  // (d) top-k by (dist, column): running sorted list, one (key) per lane
+  uint64_t best = ~0ull;  // lanes >= k never receive real entries
+  for (uint32_t b0 = 0; b0 < C; b0 += 32) {
+    const uint32_t c = b0 + lane;
+    uint64_t key = c < C ? dc_key(cd[c], c) : ~0ull;
+    const uint64_t tail = __shfl_sync(0xFFFFFFFFu, best, k - 1);
+    if (!__any_sync(0xFFFFFFFFu, key < tail)) continue;
+    // sort the chunk ascending
+    for (uint32_t kk = 2; kk <= 32; kk <<= 1)
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, key, j);
+        const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
+        if ((lower == up) ? (o < key) : (o > key)) key = o;
+      }
+    // merge: min(best[i], chunk[31 - i]) is bitonic and holds the 32 smallest
+    const uint64_t rev = __shfl_sync(0xFFFFFFFFu, key, 31 - lane);
+    best = rev < best ? rev : best;
+    for (uint32_t j = 16; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, best, j);
+      const bool lower = (lane & j) == 0;
+      if (lower ? (o < best) : (o > best)) best = o;
+    }
+  }
+  if (lane < k) {
+    const uint32_t col = (uint32_t)best;
+    out_graph[(uint64_t)v * k + lane] = cid[col];
+    out_dist[(uint64_t)v * k + lane] = __uint_as_float((uint32_t)(best >> 32));
+  }
+}
+
+// descent rows (slot ids) -> pass-2 forward rows in phys space with f64
+// distances (the exact path's contract for the reverse merge)
+__global__ void k_descent_to_phys(const int32_t* graph, uint32_t n, uint32_t k, const float* dist,
+                                  const uint32_t* s2p, const float* X, uint32_t dp, uint32_t* gf, double* gd) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  if (w >= (uint64_t)n) return;
+  const uint32_t v = (uint32_t)w, pv = s2p[v];
+  for (uint32_t j = 0; j < k; ++j) {
+    const int32_t u = graph[(uint64_t)v * k + j];
+    const bool ok = u >= 0 && (uint32_t)u != v && !isinf(dist[(uint64_t)v * k + j]);  // warp-uniform
+    if (!ok) {
+      if (lane == 0) gf[(uint64_t)pv * k + j] = kSentinel;
+      continue;
+    }
+    const uint32_t pu = s2p[u];
+    double acc = 0.0;
+    for (uint32_t col = lane * 4; col < dp; col += 128)
+      acc = sq4(ldg_nc_f4(X + (uint64_t)pu * dp + col), *reinterpret_cast<const float4*>(X + (uint64_t)pv * dp + col),
+                acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      gf[(uint64_t)pv * k + j] = pu;
+      gd[(uint64_t)pv * k + j] = acc;
+    }
+  }
+}
+
+}  // namespace
+
+// Global NN-descent graph over slots [0, n): fills gf/gd (phys rows, phys ids,
+// f64 distances, SENTINEL for unfilled) like knn_device does for the exact path.
+void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t rounds, uint32_t sample, uint32_t* gf,
+                    double* gd, cudaStream_t st) {
+  if (n64 < 3) throw Error(GRAB_ERR_VALUE, "descent needs at least 3 nodes");
+  if (k > 32) throw Error(GRAB_ERR_VALUE, "descent supports k_g <= 32");
+  if (n64 >= 0x7FFFFFFFull) throw Error(GRAB_ERR_VALUE, "descent supports n < 2^31");
+  const uint32_t n = (uint32_t)n64;
+  const uint64_t nk = (uint64_t)n * k;
+  ScratchD S(st);
+  // ---- init: graph = rng.integers(0, n - 1, (n, k)); += 1 where >= row
+  const Pcg64 g0 = pcg64_from_pair(ix.params.rng_seed, 1);
+  const JumpPow2 jt = make_pow2();
+  u128* djt = S.alloc<u128>(128);
+  GRAB_CUDA(cudaMemcpyAsync(djt, jt.a, sizeof(jt.a), cudaMemcpyHostToDevice, st));
+  GRAB_CUDA(cudaMemcpyAsync(djt + 64, jt.g, sizeof(jt.g), cudaMemcpyHostToDevice, st));
+  const uint32_t total = n - 1;                      // exclusive high n-1 -> values 0..n-2
+  const uint32_t thresh = (uint32_t)((0x100000000ull - total) % total);
+  int32_t* graph = S.alloc<int32_t>(nk);
+  uint64_t consumed_out = 0;
+  {
+    uint64_t n_words = nk + nk / 64 + 4096;
+    for (int attempt = 0;; ++attempt) {
+      const uint64_t n_out = (n_words + 1) / 2;
+      n_words = 2 * n_out;
+      uint32_t* flag = S.alloc<uint32_t>(n_words + 1);
+      uint32_t* val = S.alloc<uint32_t>(n_words);
+      uint32_t* pos = S.alloc<uint32_t>(n_words + 1);
+      unsigned long long* last = S.alloc<unsigned long long>(1);
+      GRAB_CUDA(cudaMemsetAsync(last, 0xFF, 8, st));
+      const uint64_t nthr = div_up(n_out, kOutPerThread);
+      k_init_words<<<(unsigned)div_up(nthr, 128), 128, 0, st>>>(g0.state, g0.inc, djt, djt + 64, n_out, total,
+                                                                thresh, flag, val);
+      GRAB_CHECK_LAUNCH();
+      GRAB_CUDA(cudaMemsetAsync(flag + n_words, 0, 4, st));
+      exclusive_scan_u32(flag, pos, n_words + 1, st);
+      uint32_t acc = 0;
+      GRAB_CUDA(cudaMemcpyAsync(&acc, pos + n_words, 4, cudaMemcpyDeviceToHost, st));
+      GRAB_CUDA(cudaStreamSynchronize(st));
+      if (acc < nk) {
+        if (attempt > 4) throw Error(GRAB_ERR_CUDA, "descent init: rejection stream too long");
+        n_words = n_words * 2;
+        continue;
+      }
+      k_init_scatter<<<(unsigned)div_up(n_words, 256), 256, 0, st>>>(n_words, flag, pos, val, nk, k, graph, last);
+      GRAB_CHECK_LAUNCH();
+      unsigned long long lw = 0;
+      GRAB_CUDA(cudaMemcpyAsync(&lw, last, 8, cudaMemcpyDeviceToHost, st));
+      GRAB_CUDA(cudaStreamSynchronize(st));
+      consumed_out = (lw + 2) / 2;  // words 0..lw used -> ceil((lw + 1) / 2) outputs
+      break;
+    }
+  }
+  // generator state after the fill: the bitgen's own 32-bit buffer is untouched (empty)
+  HostPcg hg;
+  {
+    const Jump j = jump_by(jt.a, jt.g, consumed_out);
+    hg.state = j.a * g0.state + j.g * g0.inc;
+    hg.inc = g0.inc;
+  }
+  float* dist = S.alloc<float>(nk);
+  k_edge_dists<<<(unsigned)div_up(div_up(nk, 4) * 32, 256), 256, 0, st>>>(graph, nk, k, ix.slot2phys, ix.X, ix.dp,
+                                                                         dist);
+  GRAB_CHECK_LAUNCH();
+  // ---- rounds
+  const uint32_t s = std::min(sample, k);
+  const uint32_t J = 2 * k, nhop = std::min(2 * s, J);
+  const uint32_t C = J + nhop * J;
+  uint32_t H = 1;
+  while (H < C + C / 2) H <<= 1;  // id hash at load <= 2/3
+  if (H > 65536) throw Error(GRAB_ERR_VALUE, "descent candidate set too large");
+  int32_t* joint = S.alloc<int32_t>((uint64_t)n * J);
+  int32_t* g2 = S.alloc<int32_t>(nk);
+  float* d2 = S.alloc<float>(nk);
+  uint64_t* key2 = S.alloc<uint64_t>(nk);
+  uint64_t* key2s = S.alloc<uint64_t>(nk);
+  uint32_t* dst = S.alloc<uint32_t>(nk);
+  uint32_t* dsts = S.alloc<uint32_t>(nk);
+  uint64_t* key2t = S.alloc<uint64_t>(nk);
+  uint32_t* dstt = S.alloc<uint32_t>(nk);
+  uint32_t* cnt = S.alloc<uint32_t>(n + 1);
+  uint32_t* off = S.alloc<uint32_t>(n + 1);
+  uint32_t* dhop = S.alloc<uint32_t>(J);
+  int end_bit = 1;
+  while ((1ull << end_bit) <= n) ++end_bit;
+  constexpr int WPB = 2;
+  const size_t smem = (size_t)WPB * (C * 10 + H * 8);
+  GRAB_CUDA(cudaFuncSetAttribute(k_descent<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (uint32_t r = 0; r < rounds; ++r) {
+    // reverse top-k: stable sort by (dist, src), then by dst
+    k_rev_keys<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(graph, dist, nk, k, n, key2, dst);
+    GRAB_CHECK_LAUNCH();
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, key2, key2s, dst, dstt, (int)nk, 0, 64, st);
+    size_t tmp2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp2, dstt, dsts, key2s, key2t, (int)nk, 0, end_bit, st);
+    void* t = S.alloc<uint8_t>(std::max(tmp, tmp2));
+    GRAB_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key2, key2s, dst, dstt, (int)nk, 0, 64, st));
+    GRAB_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp2, dstt, dsts, key2s, key2t, (int)nk, 0, end_bit, st));
+    GRAB_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * 4, st));
+    k_count_dst<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(dsts, nk, n, cnt);
+    GRAB_CHECK_LAUNCH();
+    exclusive_scan_u32(cnt, off, n + 1, st);
+    k_joint<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(graph, n, k, dsts, key2t, off, nk, joint);
+    GRAB_CHECK_LAUNCH();
+    k_joint_rev<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(n, k, dsts, key2t, off, nk, joint);
+    GRAB_CHECK_LAUNCH();
+    const std::vector<uint32_t> perm = hg.permutation(J);
+    GRAB_CUDA(cudaMemcpyAsync(dhop, perm.data(), nhop * 4, cudaMemcpyHostToDevice, st));
+    k_descent<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem, st>>>(joint, n, k, dhop, nhop, ix.slot2phys, ix.X,
+                                                                     ix.dp, C, H, g2, d2);
+    GRAB_CHECK_LAUNCH();
+    std::swap(graph, g2);
+    std::swap(dist, d2);
+    GRAB_CUDA(cudaStreamSynchronize(st));  // `perm` and the scratch stay valid across the round
+  }
+  k_descent_to_phys<<<(unsigned)div_up((uint64_t)n * 32, 256), 256, 0, st>>>(graph, n, k, dist, ix.slot2phys, ix.X,
+                                                                            ix.dp, gf, gd);
+  GRAB_CHECK_LAUNCH();
+  GRAB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace grab

@@ -72,11 +72,11 @@ class StoreView:
 class GraphIndex:
     """Owning handle of one device index (one B200)."""
 
-    def __init__(self, dim: int, capacity: int, params: BuildParams, device: int = 0):
+    def __init__(self, dim: int, capacity: int, params: BuildParams, device: int = 0, global_pass: str = "auto"):
         self.params = params
         self.device = device
         h = C.c_void_p()
-        bp = to_c_params(params)
+        bp = to_c_params(params, global_pass)
         L.check(L.lib.grab_create(device, dim, capacity, C.byref(bp), C.byref(h)))
         self._h = h
         self._dim = dim
@@ -181,15 +181,24 @@ class GraphIndex:
         return self._cached("meta", self._read_meta)
 
 
-def to_c_params(p: BuildParams) -> L.BuildParamsC:
+GLOBAL_PASS = {"auto": 0, "exact": 1, "descent": 2}
+
+
+def to_c_params(p: BuildParams, global_pass: str = "auto") -> L.BuildParamsC:
+    """``global_pass`` (not a reference field): pass-2 candidate graph -- "auto" is the
+    reference rule (exact kNN iff n <= 100 000, else NN-descent; builder.py:379-391)."""
+    if global_pass not in GLOBAL_PASS:
+        raise ValueError(f"unknown global_pass: {global_pass!r}")
     return L.BuildParamsC(k_max=p.k_max, k_local=p.k_local, bucket_capacity=p.bucket_capacity,
+                          global_pass=GLOBAL_PASS[global_pass],
                           proximal_fraction=float(p.proximal_fraction), proximal_window=float(p.proximal_window),
                           alpha=float(p.alpha), rng_seed=int(p.rng_seed))
 
 
-def create_index(dim: int, capacity: int, params: BuildParams, device: int = 0) -> GraphIndex:
+def create_index(dim: int, capacity: int, params: BuildParams, device: int = 0,
+                 global_pass: str = "auto") -> GraphIndex:
     """create_index (layout.py:250-257): empty device index of fixed capacity."""
-    return GraphIndex(dim, capacity, params, device)
+    return GraphIndex(dim, capacity, params, device, global_pass)
 
 
 def import_state(index: GraphIndex, X, scalars, adjacency, boundaries, index_to_bucket, bucket_to_index,

@@ -126,3 +126,29 @@ def test_build_recall_parity_with_reference(g):
         rb = np.mean([beam.recall(b.slots[i, :b.counts[i]], truth[i, :tc[i]], 10) for i in range(len(Q))])
         print(f"sel {sel}: recall gpu-built {ra:.4f} reference-built {rb:.4f}")
         assert abs(ra - rb) <= 0.005 or ra > rb
+
+
+@pytest.mark.parametrize("kg,rounds,key", [(8, 0, "rows0"), (32, 3, "rows")])
+def test_nn_descent_global_pass_matches_reference(g, golden, kg, rounds, key):
+    """build_global_graph above the exact limit (builder.py:379-393): random init from
+    default_rng([seed, 1]) regenerated on the device, numpy-shuffle hop columns,
+    descent rounds and the reverse merge -- every global row identical to the
+    reference's (golden from the live reference, exact_limit=0)."""
+    want = golden("descent")[key]
+    r = np.random.default_rng(9)
+    V = r.standard_normal((2000, 16)).astype(np.float32)
+    S = r.random(2000, dtype=np.float32)
+    _, rep, dr = g.build_index(V, S, g.BuildParams(), k_g=kg, refine_rounds=rounds, return_draft=True,
+                               global_pass="descent")
+    assert rep.global_pass == "descent"
+    assert np.array_equal(dr.global_rows, want)
+
+
+def test_auto_global_pass_follows_reference_limit(g):
+    r = np.random.default_rng(1)
+    V = r.standard_normal((3000, 8)).astype(np.float32)
+    S = r.random(3000, dtype=np.float32)
+    _, rep = g.build_index(V, S, g.BuildParams(bucket_capacity=1000))
+    assert rep.global_pass == "exact"  # n <= EXACT_GLOBAL_LIMIT (builder.py:33)
+    _, rep = g.build_index(V, S, g.BuildParams(bucket_capacity=1000), global_pass="descent")
+    assert rep.global_pass == "descent"
