@@ -133,7 +133,7 @@ __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15
 // {f64 distance, slot, phys | kExpanded} kept sorted by (distance, slot), so a
 // merge moves one LDS.128/STS.128 per displaced entry.
 struct WarpLayout {
-  uint32_t qe, cd, cs, cp, rr, dd, fr, bytes;
+  uint32_t qe, cd, cs, cp, rr, dd, fr, q, bytes;
 };
 
 __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
@@ -153,6 +153,8 @@ __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
   o += align16(s.dsz * 4);
   l.fr = o;
   o += align16(s.width * 4);
+  l.q = o;  // query staging for wide rows (QueryRegs, NC >= 4)
+  o += s.qbytes;
   l.bytes = o;
   return l;
 }
@@ -166,18 +168,31 @@ __device__ __forceinline__ uint4 qe_pack(double d, uint32_t s, uint32_t p) {
 }
 
 // ---------------------------------------------------------------- distances
+// The query, one float4 per lane per 128-float chunk. Up to 2 chunks it lives
+// in registers; wider rows (NC >= 4, e.g. d = 960) are staged in the warp's
+// shared memory and read per chunk, so the row being scored keeps the
+// registers (in registers the compiler also holds the f64 upcast: 16 regs/chunk).
 template <int NC>
 struct QueryRegs {
-  float4 q[NC];
+  static constexpr bool kShared = NC >= 4;
+  float4 q[kShared ? 1 : NC];
+  const float4* sq;
+  __device__ __forceinline__ float4 get(int c) const { return kShared ? sq[c * 32 + lane_id()] : q[c]; }
 };
 
 template <int NC>
-__device__ __forceinline__ void load_query(QueryRegs<NC>& r, const float* q, uint32_t dp) {
+__device__ __forceinline__ void load_query(QueryRegs<NC>& r, const float* q, uint32_t dp, float4* stage) {
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const uint32_t col = (c * 32 + lane_id()) * 4;
-    r.q[c] = col < dp ? *reinterpret_cast<const float4*>(q + col) : make_float4(0, 0, 0, 0);
+    const float4 v = col < dp ? *reinterpret_cast<const float4*>(q + col) : make_float4(0, 0, 0, 0);
+    if constexpr (QueryRegs<NC>::kShared)
+      stage[c * 32 + lane_id()] = v;
+    else
+      r.q[c] = v;
   }
+  r.sq = stage;
+  __syncwarp();
 }
 
 template <int NC>
@@ -219,7 +234,7 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
     for (int g = 0; g < G; ++g) {
       double acc = 0.0;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc = sq4(x[g][c], qr.q[c], acc);
+      for (int c = 0; c < NC; ++c) acc = sq4(x[g][c], qr.get(c), acc);
       part[g] = acc;
     }
     const double v = reduce_scatter<G>(part);
@@ -539,7 +554,8 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
     bool overflow = false;
     if (a.n_live > 0 && a.m > 0) {
       QueryRegs<NC> qr;
-      load_query<NC>(qr, a.qphys ? a.X + (uint64_t)a.qphys[qi] * a.dp : a.Q + (uint64_t)qi * a.dp, a.dp);
+      load_query<NC>(qr, a.qphys ? a.X + (uint64_t)a.qphys[qi] * a.dp : a.Q + (uint64_t)qi * a.dp, a.dp,
+                     (float4*)(base + sh.o_q));
       const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f);
       const uint32_t hi_b = bucket_of_f32(a.bound, a.m, hi_f);
       Visited vis;
@@ -791,8 +807,11 @@ static uint32_t ceil_log2(uint64_t x) {
   return l;
 }
 
-SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst) {
+SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst,
+                       uint32_t dp) {
   SearchShape s;
+  const uint32_t nc = (dp + 127) / 128;
+  s.qbytes = nc > 2 ? (nc <= 4 ? 4u : 8u) * 512u : 0u;  // QueryRegs<NC>::kShared staging
   s.itopk = itopk;
   s.width = width;
   const uint32_t fan = width * k_max;
@@ -812,6 +831,7 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   s.o_rr = l.rr;
   s.o_dd = l.dd;
   s.o_fr = l.fr;
+  s.o_q = l.q;
   s.warp_bytes = l.bytes;
   return s;
 }
@@ -878,7 +898,7 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);
   a.adja = ix.adja;
-  SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false);
+  SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp);
   DBufLite tables, big_tables, ovfb;
   ovfb.ensure((a.nwork + 1) * sizeof(uint32_t), st);
   uint32_t* ovf = (uint32_t*)ovfb.p;
@@ -888,7 +908,7 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
   launch(a, sh, ix.num_sms, st, tables, ~0ull);
-  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true);
+  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true, a.dp);
   SearchArgs b = a;
   b.qmap = a.ovf_list;
   b.nwork_dev = ovf;
