@@ -32,6 +32,12 @@ PRESETS = {
     "cfg1": dict(n=100_000, dim=128, cap=6250, nq=1000, sel=0.10),
     "cfg2": dict(n=1_000_000, dim=128, cap=10_000, nq=10_000, sel=0.10),
     "cfg3": dict(n=1_000_000, dim=960, cap=10_000, nq=10_000, sel=0.10),
+    # dynamic: build 1M, then append-only insert 1M in 100K batches with a 10K-query
+    # batch at 10 % after each (BASELINE configs[3])
+    "cfg4": dict(n=1_000_000, dim=128, cap=10_000, nq=10_000, sel=0.10, inserts=1_000_000, batch=100_000),
+    # bucket-range sharded Deep100M shape: 12.5M x 96 rows PER GPU (100M at 8 GPUs),
+    # 12.5K range queries per GPU (100K at 8), weak scaling (BASELINE configs[4])
+    "cfg5": dict(n=12_500_000, dim=96, cap=10_000, nq=12_500, sel=0.10),
 }
 GRID = [(32, 1, 50), (32, 2, 50), (48, 2, 50), (64, 2, 50), (64, 4, 50), (96, 4, 50), (128, 4, 50), (192, 4, 50),
         (128, 4, 100), (160, 4, 100), (192, 4, 100), (224, 4, 100), (256, 4, 100), (192, 2, 100), (256, 2, 150),
@@ -178,6 +184,155 @@ def cpu_search_qps(idx, Q, lo, hi, seeds, point, procs: int, steps: int):
     return len(Q) * steps / el, el, slots
 
 
+# ------------------------------------------------------------------ cfg4 / cfg5
+def _timed(fn, stream):
+    """CUDA-event time (ms) of fn() on `stream`, synchronized on both sides."""
+    import torch
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), out
+
+
+def _max_over_ranks(v, dist, dev):
+    if not dist:
+        return v
+    import torch
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_dynamic(args, cfg, rank, world, local, dist):
+    """cfg4: build 1M (N_cap = 2M), then insert 1M as 10 x 100K append-only batches;
+    after each batch a 10K-query batch at 10 % selectivity at a fixed operating
+    point, with recall against the exact filtered oracle over the grown index.
+    The line's metric is insert vectors/s over all batches (device-resident
+    batches, event-timed); per-batch recall / QPS ride along."""
+    import torch
+    import paper_2604_16402_b200 as g
+    from paper_2604_16402_b200 import datasets as ds
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n, dim, cap, nq, sel = cfg["n"], cfg["dim"], cfg["cap"], cfg["nq"], cfg["sel"]
+    total, batch = args.inserts or cfg["inserts"], cfg["batch"]
+    X, S = ds.gen_lowrank(n + total, dim, seed=0)
+    params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
+    t0 = time.perf_counter()
+    gi, brep = g.build_index(X[:n], S[:n], params, capacity=n + total, device=local, global_pass=args.global_pass)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    Q = ds.lowrank_queries(nq, dim, seed=1)
+    Qd = torch.from_numpy(Q).to(dev)
+    sp = g.SearchParams(k=10, itopk=args.itopk, search_width=4, max_iterations=100)
+    rounds, ins_ms = [], 0.0
+    with ClockSampler(local) as clk:
+        for b0 in range(n, n + total, batch):
+            Xi = torch.from_numpy(X[b0:b0 + batch]).to(dev)
+            Si = torch.from_numpy(S[b0:b0 + batch]).to(dev)
+            ms, rep = _timed(lambda: g.insert_batch(gi, Xi, Si), stream)
+            ins_ms += ms
+            lo, hi = ds.range_arrays(ds.generate_ranges(S[:b0 + batch], sel, nq, b0))
+            truth, _, tc = g.brute_force_arrays(gi, Q, lo, hi, 10)
+            r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0, stats=False)
+            rec = ds.batch_recall(r.slots, r.counts, truth, tc, 10)
+            lod, hid = torch.from_numpy(lo).to(dev), torch.from_numpy(hi).to(dev)
+            for _ in range(args.warmup):
+                g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False)
+            sms, _ = _timed(lambda: [g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False)
+                                     for _ in range(args.steps)], stream)
+            rounds.append({"rows": b0 + batch, "insert_s": round(ms / 1e3, 4), "recall_at_10": round(rec, 4),
+                           "qps": round(nq * args.steps / (sms / 1e3), 1),
+                           "forced_links": int(rep.forced_links), "rewired_rows": len(rep.rewired_rows)})
+    ins_ms = _max_over_ranks(ins_ms, dist, dev)
+    vps = world * total / (ins_ms / 1e3)
+    line = {"metric": "insert vectors/s (cfg4 dynamic)", "value": round(vps, 1), "unit": "vectors/s",
+            "n_gpus": world, "steps": total // batch, "warmup": args.warmup,
+            "ms_per_step": round(ins_ms / (total // batch), 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 accumulate / f32 storage",
+            "data": "synthetic (low-rank-16; 2M rows drawn once, first 1M built, rest inserted)",
+            "config": {"workload": f"cfg4: build {n}x{dim} then insert {total} in {batch}-row batches, {nq} "
+                                   f"queries at {int(sel * 100)}% after each (itopk {args.itopk}, width 4, 100 it)",
+                       "index": "replicated per GPU" if world > 1 else "single GPU",
+                       "global_pass": brep.global_pass},
+            "build_s": round(build_s, 3), "rounds": rounds, "gpu_launches": None, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_sharded(args, cfg, rank, world, local, dist):
+    """cfg5: bucket-range sharded index, weak scaling. Rank r generates its own
+    n rows (low-rank-16 with seed (0, r)) whose scalars are uniform in its range
+    [r/N, (r+1)/N) -- distributed exactly like one N*n-row draw split by scalar
+    quantiles -- builds its shard, and serves N*nq range queries (10 %
+    selectivity over [0, 1)) through route -> search -> pack -> NCCL
+    all-to-all -> merge. Recall is against the sharded exact pipeline (the
+    single-index brute force, id for id)."""
+    import torch
+    import paper_2604_16402_b200 as g
+    from paper_2604_16402_b200 import datasets as ds
+    from paper_2604_16402_b200 import shard as sh
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n, dim, cap, nq, sel = cfg["n"], cfg["dim"], cfg["cap"], cfg["nq"], cfg["sel"]
+    X, S = ds.gen_lowrank(n, dim, seed=1000 + rank)
+    S = ((S + np.float32(rank)) / np.float32(world)).astype(np.float32)
+    gid = np.arange(n, dtype=np.int64) + rank * n
+    params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    idx, brep = sh.ShardedIndex.build(X, S, gid, params, rank=rank, world=world, device=local,
+                                      global_pass=args.global_pass)
+    torch.cuda.synchronize()
+    build_s = _max_over_ranks(time.perf_counter() - t0, dist, dev)
+    del X
+    NQ = nq * world
+    Q = ds.lowrank_queries(NQ, dim, seed=1)
+    gq = np.random.default_rng([7, 3, int(sel * 1e6)])
+    lo = gq.random(NQ) * (1.0 - sel)
+    hi = lo + sel
+    Qd = torch.from_numpy(Q).to(dev)
+    truth = idx.search(Qd, lo, hi, g.SearchParams(k=10, itopk=16), exact=True)
+    sp = g.SearchParams(k=10, itopk=args.itopk, search_width=4, max_iterations=100)
+    for _ in range(args.warmup):
+        res = idx.search(Qd, lo, hi, sp, seed_base=0)
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        ms, res = _timed(lambda: [idx.search(Qd, lo, hi, sp, seed_base=0) for _ in range(args.steps)][-1], stream)
+    ms = _max_over_ranks(ms, dist, dev)
+    tr_s, tr_c = truth.slots.cpu().numpy(), truth.counts.cpu().numpy()
+    rs, rc = res.slots.cpu().numpy(), res.counts.cpu().numpy()
+    rec_local = ds.batch_recall(rs, rc, tr_s, tr_c, 10) if len(rc) else float("nan")
+    rec = rec_local
+    if dist:
+        t = torch.tensor([rec_local * len(rc), len(rc)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        rec = float(t[0] / t[1])
+    qps = NQ * args.steps / (ms / 1e3)
+    line = {"metric": "range-filtered QPS (cfg5 bucket-range sharded)", "value": round(qps, 1),
+            "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 accumulate / f32 storage",
+            "data": "synthetic (low-rank-16 per shard, scalars uniform in the shard's range)",
+            "config": {"workload": f"cfg5: {n}x{dim} rows per GPU ({n * world} total), {NQ} range queries at "
+                                   f"{int(sel * 100)}% selectivity, k=10, itopk {args.itopk}",
+                       "rows_per_gpu": n, "queries": NQ, "recall_at_10": round(rec, 4),
+                       "routed_queries_rank0": int(res.routed), "index": "bucket-range sharded",
+                       "exchange": "NCCL all_to_all_single" if dist else "none (1 shard)",
+                       "global_pass": brep.global_pass},
+            "build_s": round(build_s, 3), "gpu_launches": None, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -195,6 +350,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--insert-batch", type=int, default=100_000)
+    ap.add_argument("--inserts", type=int, help="cfg4: rows inserted after the build")
+    ap.add_argument("--itopk", type=int, default=320, help="operating point of the cfg4 / cfg5 modes")
     ap.add_argument("--global-pass", default="auto", choices=["auto", "exact", "descent"],
                     help="pass-2 graph: auto = the reference rule (NN-descent above 100K rows)")
     args = ap.parse_args()
@@ -218,6 +375,10 @@ def main():
     from paper_2604_16402_b200 import datasets as ds
 
     n, dim, cap, nq, sel = cfg["n"], cfg["dim"], cfg["cap"], cfg["nq"], cfg["sel"]
+    if args.config == "cfg4" and args.impl == "grab":
+        return run_dynamic(args, cfg, rank, world, local, dist)
+    if args.config == "cfg5" and args.impl == "grab":
+        return run_sharded(args, cfg, rank, world, local, dist)
     X, S = ds.gen_lowrank(n, dim, seed=0)
     Qall = ds.lowrank_queries(nq * world, dim, seed=1)
     ranges = ds.generate_ranges(S, sel, nq * world, 0)
