@@ -235,6 +235,7 @@ def run_dynamic(args, cfg, rank, world, local, dist):
             Si = torch.from_numpy(S[b0:b0 + batch]).to(dev)
             ms, rep = _timed(lambda: g.insert_batch(gi, Xi, Si), stream)
             ins_ms += ms
+            print(f"[cfg4] inserted {b0 + batch} rows in {ms:.1f} ms", file=sys.stderr, flush=True)
             lo, hi = ds.range_arrays(ds.generate_ranges(S[:b0 + batch], sel, nq, b0))
             truth, _, tc = g.brute_force_arrays(gi, Q, lo, hi, 10)
             r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0, stats=False)
@@ -244,6 +245,7 @@ def run_dynamic(args, cfg, rank, world, local, dist):
                 g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False)
             sms, _ = _timed(lambda: [g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False)
                                      for _ in range(args.steps)], stream)
+            print(f"[cfg4] rows {b0 + batch}: recall {rec:.4f}", file=sys.stderr, flush=True)
             rounds.append({"rows": b0 + batch, "insert_s": round(ms / 1e3, 4), "recall_at_10": round(rec, 4),
                            "qps": round(nq * args.steps / (sms / 1e3), 1),
                            "forced_links": int(rep.forced_links), "rewired_rows": len(rep.rewired_rows)})
@@ -280,7 +282,7 @@ def run_sharded(args, cfg, rank, world, local, dist):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     n, dim, cap, nq, sel = cfg["n"], cfg["dim"], cfg["cap"], cfg["nq"], cfg["sel"]
-    X, S = ds.gen_lowrank(n, dim, seed=1000 + rank)
+    X, S = ds.gen_lowrank(n, dim, seed=1000 + rank, w_seed=0)
     S = ((S + np.float32(rank)) / np.float32(world)).astype(np.float32)
     gid = np.arange(n, dtype=np.int64) + rank * n
     params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)

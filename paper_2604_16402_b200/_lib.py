@@ -96,6 +96,8 @@ _SIGS = {
     "grab_shard_pack": (C.c_int, [u64, P, P, P, P, u32, u32, u32, P, P, P]),
     "grab_merge_topk": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, P]),
     "grab_derive_seeds": (C.c_int, [u64, P, u64, P]),
+    "grab_scc_count": (C.c_int, [P, u64, P]),
+    "grab_scc_count_raw": (C.c_int, [P, u64, u32, u64, P]),
 }
 
 

@@ -569,3 +569,33 @@ extern "C" int grab_derive_seeds(uint64_t base, const uint32_t* ordinals, uint64
     for (uint64_t i = 0; i < n; ++i) out[i] = derive_query_seed(base, ordinals[i]);
   });
 }
+
+namespace grab {
+uint64_t scc_count_device(const uint32_t* adj, uint32_t n, uint32_t K, cudaStream_t st);  // scc.cu
+}
+
+extern "C" int grab_scc_count(const grab_index* h, uint64_t live_count, uint64_t* out) {
+  return guarded([&] {
+    check_handle(h);
+    const DevIndex& ix = h->ix;
+    set_device(ix);
+    const uint64_t n = live_of(ix, live_count);
+    if (n >= 0xFFFFFFFFull) throw Error(GRAB_ERR_VALUE, "too many rows");
+    cudaStream_t st = ix.stream;
+    DBuf a(std::max<uint64_t>(n, 1) * ix.params.k_max * 4, st);
+    adjacency_phys_to_slot(ix, a.as<uint32_t>(), 0, n);
+    *out = scc_count_device(a.as<uint32_t>(), (uint32_t)n, ix.params.k_max, st);
+  });
+}
+
+extern "C" int grab_scc_count_raw(const uint32_t* adjacency, uint64_t rows, uint32_t k_max, uint64_t live_count,
+                                  uint64_t* out) {
+  return guarded([&] {
+    const uint64_t n = std::min(rows, live_count);
+    if (n >= 0xFFFFFFFFull) throw Error(GRAB_ERR_VALUE, "too many rows");
+    cudaStream_t st = nullptr;
+    DBuf a(std::max<uint64_t>(n, 1) * k_max * 4, st);
+    GRAB_CUDA(cudaMemcpyAsync(a.p, adjacency, n * k_max * 4, cudaMemcpyHostToDevice, st));
+    *out = scc_count_device(a.as<uint32_t>(), (uint32_t)n, k_max, st);
+  });
+}

@@ -30,9 +30,15 @@ def gen_synthetic(n: int, d: int, distribution: str = "gaussian", rng_seed: int 
     return v, g.random(n, dtype=np.float32)
 
 
-def gen_lowrank(n: int, d: int, seed: int = 0, rank: int = 16, noise: float = 0.05):
+def gen_lowrank(n: int, d: int, seed: int = 0, rank: int = 16, noise: float = 0.05, w_seed: int | None = None):
+    """``w_seed`` (sharded data): draw the rank-16 basis from default_rng(w_seed)
+    and only the coefficients / noise / scalars from ``seed``, so every shard
+    shares the query distribution's subspace (lowrank_queries uses seed 0)."""
     g = np.random.default_rng(seed)
-    W = (g.standard_normal((rank, d)) / 4).astype(np.float32)
+    if w_seed is None:
+        W = (g.standard_normal((rank, d)) / 4).astype(np.float32)
+    else:
+        W = (np.random.default_rng(w_seed).standard_normal((rank, d)) / 4).astype(np.float32)
     Z = g.standard_normal((n, rank)).astype(np.float32)
     E = g.standard_normal((n, d)).astype(np.float32)
     X = (Z @ W + np.float32(noise) * E).astype(np.float32)
