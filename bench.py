@@ -227,7 +227,8 @@ def run_dynamic(args, cfg, rank, world, local, dist):
     build_s = time.perf_counter() - t0
     Q = ds.lowrank_queries(nq, dim, seed=1)
     Qd = torch.from_numpy(Q).to(dev)
-    sp = g.SearchParams(k=10, itopk=args.itopk, search_width=4, max_iterations=100)
+    itopk = args.itopk or 320
+    sp = g.SearchParams(k=10, itopk=itopk, search_width=4, max_iterations=100)
     rounds, ins_ms = [], 0.0
     with ClockSampler(local) as clk:
         for b0 in range(n, n + total, batch):
@@ -257,7 +258,7 @@ def run_dynamic(args, cfg, rank, world, local, dist):
             "vs_baseline": None, "dtype": "f64 accumulate / f32 storage",
             "data": "synthetic (low-rank-16; 2M rows drawn once, first 1M built, rest inserted)",
             "config": {"workload": f"cfg4: build {n}x{dim} then insert {total} in {batch}-row batches, {nq} "
-                                   f"queries at {int(sel * 100)}% after each (itopk {args.itopk}, width 4, 100 it)",
+                                   f"queries at {int(sel * 100)}% after each (itopk {itopk}, width 4, 100 it)",
                        "index": "replicated per GPU" if world > 1 else "single GPU",
                        "global_pass": brep.global_pass},
             "build_s": round(build_s, 3), "rounds": rounds, "gpu_launches": None, "clocks": clk.summary()}
@@ -289,7 +290,7 @@ def run_sharded(args, cfg, rank, world, local, dist):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     idx, brep = sh.ShardedIndex.build(X, S, gid, params, rank=rank, world=world, device=local,
-                                      global_pass=args.global_pass)
+                                      global_pass=args.global_pass, refine_rounds=args.refine_rounds or 10)
     torch.cuda.synchronize()
     build_s = _max_over_ranks(time.perf_counter() - t0, dist, dev)
     del X
@@ -300,7 +301,8 @@ def run_sharded(args, cfg, rank, world, local, dist):
     hi = lo + sel
     Qd = torch.from_numpy(Q).to(dev)
     truth = idx.search(Qd, lo, hi, g.SearchParams(k=10, itopk=16), exact=True)
-    sp = g.SearchParams(k=10, itopk=args.itopk, search_width=4, max_iterations=100)
+    itopk = args.itopk or 512
+    sp = g.SearchParams(k=10, itopk=itopk, search_width=4, max_iterations=150)
     for _ in range(args.warmup):
         res = idx.search(Qd, lo, hi, sp, seed_base=0)
     if dist:
@@ -323,7 +325,8 @@ def run_sharded(args, cfg, rank, world, local, dist):
             "vs_baseline": None, "dtype": "f64 accumulate / f32 storage",
             "data": "synthetic (low-rank-16 per shard, scalars uniform in the shard's range)",
             "config": {"workload": f"cfg5: {n}x{dim} rows per GPU ({n * world} total), {NQ} range queries at "
-                                   f"{int(sel * 100)}% selectivity, k=10, itopk {args.itopk}",
+                                   f"{int(sel * 100)}% selectivity, k=10, itopk {itopk} / width 4 / 150 it, "
+                                   f"NN-descent rounds {args.refine_rounds or 10}",
                        "rows_per_gpu": n, "queries": NQ, "recall_at_10": round(rec, 4),
                        "routed_queries_rank0": int(res.routed), "index": "bucket-range sharded",
                        "exchange": "NCCL all_to_all_single" if dist else "none (1 shard)",
@@ -353,7 +356,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--insert-batch", type=int, default=100_000)
     ap.add_argument("--inserts", type=int, help="cfg4: rows inserted after the build")
-    ap.add_argument("--itopk", type=int, default=320, help="operating point of the cfg4 / cfg5 modes")
+    ap.add_argument("--itopk", type=int, help="operating point of the cfg4 / cfg5 modes (320 / 512)")
+    ap.add_argument("--refine-rounds", type=int, help="NN-descent rounds (reference default 3; cfg5 uses 10)")
     ap.add_argument("--global-pass", default="auto", choices=["auto", "exact", "descent"],
                     help="pass-2 graph: auto = the reference rule (NN-descent above 100K rows)")
     args = ap.parse_args()
