@@ -302,16 +302,6 @@ __device__ __forceinline__ uint32_t rank_in_queue(const uint4* qe, uint32_t L, d
   return pos;
 }
 
-// #{j < n : rr[j] <= i} over the nondecreasing rank array rr.
-__device__ __forceinline__ uint32_t upper_rank(const uint32_t* rr, uint32_t n, uint32_t i) {
-  uint32_t pos = 0;
-  for (uint32_t step = 1u << (31 - __clz(n)); step > 0; step >>= 1) {
-    const uint32_t probe = pos + step;
-    if (probe <= n && rr[probe - 1] <= i) pos = probe;
-  }
-  return pos;
-}
-
 // CandidateQueue.admit (searcher.py:64-71): merge the nc candidates (cd, cs,
 // cp) into the queue of length L in place, truncated to itopk. Candidates that
 // cannot beat the current tail are dropped first (compacted in place); the
@@ -376,28 +366,31 @@ __device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, u
     // survivors sit in lanes [0, navail): a network over the next power of 2 sorts them first
     const uint32_t navail = min(32u, nc - b0);
     warp_sort(d, s, p, navail <= 1 ? 0 : 32 - __clz(navail - 1));
-    const uint32_t r = rank_in_queue(qe, L, d, s);
-    rr[lane] = r;
-    __syncwarp();
-    const uint32_t r0 = __shfl_sync(kFull, r, 0);
-    if (r0 < L) {
-      for (int32_t c0 = (int32_t)((L - 1) & ~31u); c0 >= (int32_t)(r0 & ~31u); c0 -= 32) {
-        const uint32_t j = (uint32_t)c0 + lane;
-        uint4 e;
-        uint32_t dst = kFull;
-        if (j < L && j >= r0) {
-          e = qe[j];
-          dst = j + upper_rank(rr, cnt, j);
-        }
-        __syncwarp();
-        if (dst < itopk) qe[dst] = e;
-        __syncwarp();
-      }
+    // final position of survivor i: i + (queue entries before it); distinct and increasing
+    const uint32_t f = lane < cnt ? lane + rank_in_queue(qe, L, d, s) : kFull;
+    const uint32_t f0 = __shfl_sync(kFull, f, 0);
+    const uint32_t newL = min(itopk, L + cnt);
+    // fill the output positions [f0, newL) chunk by chunk from the top: position
+    // pos holds survivor (#survivors before pos) if some f == pos, else queue
+    // entry pos - (#survivors before pos); every source index is <= pos, so
+    // top-down chunks read their sources before anything below is written
+    for (int32_t c0 = (int32_t)((newL - 1) & ~31u); c0 >= (int32_t)(f0 & ~31u); c0 -= 32) {
+      const uint32_t P0 = (uint32_t)c0, pos = P0 + lane;
+      const uint32_t B = __reduce_or_sync(kFull, (f >= P0 && f < P0 + 32) ? 1u << (f - P0) : 0u);
+      const uint32_t before = __popc(__ballot_sync(kFull, f < P0)) + __popc(B & ((1u << lane) - 1));
+      const bool is_c = (B >> lane) & 1u;
+      const double cdv = __shfl_sync(kFull, d, before & 31);
+      const uint32_t csv = __shfl_sync(kFull, s, before & 31);
+      const uint32_t cpv = __shfl_sync(kFull, p, before & 31);
+      const bool live = pos >= f0 && pos < newL;
+      uint4 e = make_uint4(0, 0, 0, 0);
+      if (live && !is_c) e = qe[pos - before];
+      __syncwarp();
+      if (live) qe[pos] = is_c ? qe_pack(cdv, csv, cpv) : e;
+      __syncwarp();
     }
-    if (lane < cnt && lane + r < itopk) qe[lane + r] = qe_pack(d, s, p);
-    fu = min(fu, r0);
-    L = min(itopk, L + cnt);
-    __syncwarp();
+    fu = min(fu, f0);
+    L = newL;
   }
   return L;
 }
