@@ -248,8 +248,10 @@ __device__ __forceinline__ uint64_t dc_key(float d, uint32_t col) {
 }
 
 // One descent round: one warp per node. Shared memory per warp: candidate ids
-// [C], their dedup slot [C] (u16), f32 distances [C], and a 2H-entry id hash
-// (keys) with the minimum column per key.
+// [C], their f32 distances [C] (first used as the "compute" flag) and an
+// H-entry id hash. First occurrences are found in column order: chunk by
+// chunk, the lowest lane of each id inside the chunk (match_any) inserts it,
+// and an id already present from an earlier chunk is a repeat.
 template <int WPB>
 __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint32_t n, uint32_t k,
                                                       const uint32_t* hop, uint32_t nhop, const uint32_t* s2p,
@@ -259,34 +261,31 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
   const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
   const uint32_t v = blockIdx.x * WPB + wib;
   if (v >= n) return;  // warp-uniform
-  uint8_t* base = smem + (size_t)wib * (C * 10 + H * 8);
+  uint8_t* base = smem + (size_t)wib * (C * 8 + H * 4);
   int32_t* cid = (int32_t*)base;
   float* cd = (float*)(base + C * 4);
   uint32_t* hkey = (uint32_t*)(base + C * 8);
-  uint32_t* hcol = hkey + H;
-  uint16_t* cslot = (uint16_t*)(hcol + H);
   const uint32_t J = 2 * k;
   const int32_t* jv = joint + (uint64_t)v * J;
   // (a) candidate ids: own joint row, then the joint rows of the hop sources
-  for (uint32_t i = lane; i < H; i += 32) {
-    hkey[i] = 0;
-    hcol[i] = 0xFFFFFFFFu;
-  }
+  for (uint32_t i = lane; i < H; i += 32) hkey[i] = 0;
   for (uint32_t i = lane; i < J; i += 32) cid[i] = jv[i];
   for (uint32_t h = 0; h < nhop; ++h) {
     const int32_t src = jv[hop[h]];
     for (uint32_t i = lane; i < J; i += 32) cid[J + h * J + i] = src >= 0 ? joint[(uint64_t)src * J + i] : -1;
   }
   __syncwarp();
-  // (b) first occurrence per id: hash id -> min column (warp-uniform probing)
+  // (b) first occurrence per id, in column order
   const uint32_t hmask = H - 1;
+  const float kInfF = __int_as_float(0x7F800000);
   for (uint32_t b0 = 0; b0 < C; b0 += 32) {
     const uint32_t c = b0 + lane;
     const int32_t id = c < C ? cid[c] : -1;
-    bool act = id >= 0;
+    const uint32_t same = __match_any_sync(0xFFFFFFFFu, (uint32_t)id);
+    const bool lead = id >= 0 && (uint32_t)(__ffs(same) - 1) == lane;
     uint32_t h = ((uint32_t)id * 0x9E3779B1u) & hmask;
-    uint32_t cur = act ? atomicCAS(hkey + h, 0u, (uint32_t)id + 1) : 0u;
-    bool pend = act && cur != 0u && cur != (uint32_t)id + 1;
+    uint32_t cur = lead ? atomicCAS(hkey + h, 0u, (uint32_t)id + 1) : 0u;
+    bool pend = lead && cur != 0u && cur != (uint32_t)id + 1;
     while (__any_sync(0xFFFFFFFFu, pend)) {
       if (pend) {
         h = (h + 1) & hmask;
@@ -294,12 +293,11 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
         pend = cur != 0u && cur != (uint32_t)id + 1;
       }
     }
-    if (act) atomicMin(hcol + h, c);
-    if (c < C) cslot[c] = act ? (uint16_t)h : (uint16_t)0xFFFF;
+    if (c < C) cd[c] = (lead && cur == 0u && (uint32_t)id != v) ? 0.0f : kInfF;  // 0 = compute
   }
   __syncwarp();
-  // (c) distances (inf: missing, self, repeat): 8-lane groups, 4 candidates
-  // per group per step (16 rows in flight per warp)
+  // (c) distances of the first occurrences: 8-lane groups, 4 candidates per
+  // group per step (16 rows in flight per warp)
   const uint32_t pv = s2p[v];
   const float* qrow = X + (uint64_t)pv * dp;
   const uint32_t sub = lane & 7, grp = lane >> 3;
@@ -309,13 +307,8 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t c = b0 + grp * 4 + u;
-      ok[u] = false;
-      pc[u] = 0;
-      if (c < C) {
-        const int32_t id = cid[c];
-        ok[u] = id >= 0 && (uint32_t)id != v && hcol[cslot[c]] == c;
-        if (ok[u]) pc[u] = s2p[id];
-      }
+      ok[u] = c < C && cd[c] == 0.0f;
+      pc[u] = ok[u] ? s2p[cid[c]] : 0u;
     }
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 2
@@ -333,7 +326,8 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
       acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 2);
       acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 1);
       const uint32_t c = b0 + grp * 4 + u;
-      if (c < C && sub == 0) cd[c] = ok[u] ? (float)acc[u] : __int_as_float(0x7F800000);
+      __syncwarp();
+      if (ok[u] && sub == 0) cd[c] = (float)acc[u];
     }
   }
   __syncwarp();
@@ -466,7 +460,7 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   const uint32_t J = 2 * k, nhop = std::min(2 * s, J);
   const uint32_t C = J + nhop * J;
   uint32_t H = 1;
-  while (H < C + C / 2) H <<= 1;  // id hash at load <= 2/3
+  while (H < C + C / 2) H <<= 1;  // id hash at load <= 2/3 (1088 candidates -> 2048)
   if (H > 65536) throw Error(GRAB_ERR_VALUE, "descent candidate set too large");
   int32_t* joint = S.alloc<int32_t>((uint64_t)n * J);
   int32_t* g2 = S.alloc<int32_t>(nk);
@@ -482,8 +476,8 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   uint32_t* dhop = S.alloc<uint32_t>(J);
   int end_bit = 1;
   while ((1ull << end_bit) <= n) ++end_bit;
-  constexpr int WPB = 2;
-  const size_t smem = (size_t)WPB * (C * 10 + H * 8);
+  constexpr int WPB = 4;
+  const size_t smem = (size_t)WPB * (C * 8 + H * 4);
   GRAB_CUDA(cudaFuncSetAttribute(k_descent<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (uint32_t r = 0; r < rounds; ++r) {
     // reverse top-k: stable sort by (dist, src), then by dst

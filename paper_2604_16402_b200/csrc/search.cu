@@ -535,6 +535,7 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
   const uint32_t nw = gridDim.x * wpb;
   const uint32_t dlg = 31 - __clz(sh.dsz);
   const uint32_t K = a.k_max;
+  const uint32_t kshift = (K & (K - 1)) == 0 ? 31 - __clz(K) : 0;  // power-of-two K: shifts, not divisions
   const uint32_t nwork = a.nwork_dev ? *a.nwork_dev : a.nwork;
 
   for (uint32_t item = gw; item < nwork; item += nw) {
@@ -611,7 +612,8 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
             v[t] = kSentinel;
             at[t] = make_uint2(0x7FC00000u, kNoSlot);
             if (e < fan) {
-              const uint64_t idx = (uint64_t)fr[e / K] * K + (e % K);
+              const uint32_t row = kshift ? e >> kshift : e / K;  // K = 32: row t, column lane
+              const uint64_t idx = (uint64_t)fr[row] * K + (e - row * K);
               v[t] = __ldg(a.adj + idx);
               at[t] = __ldg(reinterpret_cast<const uint2*>(a.adja) + idx);
             }
