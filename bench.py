@@ -286,11 +286,12 @@ def run_sharded(args, cfg, rank, world, local, dist):
     X, S = ds.gen_lowrank(n, dim, seed=1000 + rank, w_seed=0)
     S = ((S + np.float32(rank)) / np.float32(world)).astype(np.float32)
     gid = np.arange(n, dtype=np.int64) + rank * n
-    params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
+    # the paper's scale setting: M = K_max = 64, global pool k_g = 32
+    params = g.BuildParams(k_max=64, k_local=32, bucket_capacity=cap)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     idx, brep = sh.ShardedIndex.build(X, S, gid, params, rank=rank, world=world, device=local,
-                                      global_pass=args.global_pass, refine_rounds=args.refine_rounds or 10)
+                                      global_pass=args.global_pass, refine_rounds=args.refine_rounds or 10, k_g=32)
     torch.cuda.synchronize()
     build_s = _max_over_ranks(time.perf_counter() - t0, dist, dev)
     del X
@@ -301,8 +302,8 @@ def run_sharded(args, cfg, rank, world, local, dist):
     hi = lo + sel
     Qd = torch.from_numpy(Q).to(dev)
     truth = idx.search(Qd, lo, hi, g.SearchParams(k=10, itopk=16), exact=True)
-    itopk = args.itopk or 512
-    sp = g.SearchParams(k=10, itopk=itopk, search_width=4, max_iterations=150)
+    itopk = args.itopk or 384
+    sp = g.SearchParams(k=10, itopk=itopk, search_width=2, max_iterations=200)
     for _ in range(args.warmup):
         res = idx.search(Qd, lo, hi, sp, seed_base=0)
     if dist:
@@ -325,8 +326,8 @@ def run_sharded(args, cfg, rank, world, local, dist):
             "vs_baseline": None, "dtype": "f64 accumulate / f32 storage",
             "data": "synthetic (low-rank-16 per shard, scalars uniform in the shard's range)",
             "config": {"workload": f"cfg5: {n}x{dim} rows per GPU ({n * world} total), {NQ} range queries at "
-                                   f"{int(sel * 100)}% selectivity, k=10, itopk {itopk} / width 4 / 150 it, "
-                                   f"NN-descent rounds {args.refine_rounds or 10}",
+                                   f"{int(sel * 100)}% selectivity, k=10, K_max 64 / K_local 32 / k_g 32, itopk {itopk} / "
+                                   f"width 2 / 200 it, NN-descent rounds {args.refine_rounds or 10}",
                        "rows_per_gpu": n, "queries": NQ, "recall_at_10": round(rec, 4),
                        "routed_queries_rank0": int(res.routed), "index": "bucket-range sharded",
                        "exchange": "NCCL all_to_all_single" if dist else "none (1 shard)",
