@@ -813,7 +813,9 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   s.cmax = 1u << ceil_log2(std::max<uint64_t>(std::max(fan, want), 32));  // bitonic pads to a power of 2
   s.dsz = 1u << ceil_log2(std::max<uint64_t>(4ull * fan, 128));  // dedup table, load <= 1/4
   if (!worst) {
-    s.vlog2 = std::min<uint32_t>(15, std::max<uint32_t>(11, ceil_log2((uint64_t)itopk * 24)));
+    // sized for the visits of a wide (hash-mode) search: ~itopk * 36 at full range (1M rows, itopk 128:
+    // a 4K table overflowed every insert candidate search); a bitmap needs only nbits / 8 of it
+    s.vlog2 = std::min<uint32_t>(15, std::max<uint32_t>(12, ceil_log2((uint64_t)itopk * 48)));
   } else {
     const uint64_t bound = (uint64_t)want + (uint64_t)max_iter * fan + fan;
     s.vlog2 = std::max<uint32_t>(11, ceil_log2(bound * 4 / 3 + 1));
