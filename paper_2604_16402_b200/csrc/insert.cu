@@ -360,6 +360,12 @@ __global__ void k_heal_choose(const uint32_t* missing, uint32_t nmiss, uint64_t 
   if (lane_id() == 0) keys[t] = v == kSentinel ? ~0ull : (((unsigned long long)v << 32) | (unsigned long long)q);
 }
 
+// Forced links into one target row v, requests in q order (updater.py:301-321).
+// The row's entries, their f64 distances to v and their "stale" flag (slot
+// outside the batch) are cached per lane (entries j = lane, lane + 32; K <= 64)
+// once, so a request costs one distance (the new entry's) instead of
+// re-measuring the whole eviction region; eviction = first argmax of the
+// cached distance over [K_local, K), stale entries preferred.
 template <int NC>
 __global__ void k_heal_apply(const unsigned long long* keys, uint64_t nreq, const uint32_t* heads, uint32_t nheads,
                              uint64_t start, uint64_t end, const uint32_t* s2p, const Attr* attr, const float* X,
@@ -374,39 +380,123 @@ __global__ void k_heal_apply(const unsigned long long* keys, uint64_t nreq, cons
   uint32_t* row = adj + (uint64_t)pv * K;
   RowRegs<NC> vr;
   load_row<NC>(vr, X, dp, pv);
+  const double kNegInf = -__longlong_as_double(0x7FF0000000000000ll);
+  uint32_t e[2];
+  double d[2];
+  bool st[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t j = lane + 32 * u;
+    e[u] = j < K ? row[j] : kSentinel;
+    st[u] = false;
+    if (e[u] != kSentinel) {
+      const uint32_t s = attr[e[u]].slot;
+      st[u] = s < start || s >= end;
+    }
+  }
+  const uint32_t r0 = K > k_local ? k_local : 0;
+  // distances of the current eviction-region entries [r0, K): 8 rows in flight
+  // per round for d <= 128 (same reduction tree as row_dist), else one by one
+  d[0] = d[1] = kNegInf;
+  for (uint32_t j0 = r0; j0 < K; j0 += 8) {
+    if constexpr (NC == 1) {
+      float4 x[8];
+      bool okg[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const uint32_t j = j0 + g;
+        const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+        okg[g] = j < K && eo != kSentinel;
+        const uint32_t col = lane * 4;
+        x[g] = (okg[g] && col < dp) ? ldg_nc_f4(X + (uint64_t)eo * dp + col) : make_float4(0, 0, 0, 0);
+      }
+      double part[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) part[g] = sq4(x[g], vr.v[0], 0.0);
+      const double sum = reduce_scatter<8>(part);  // lane 4g holds entry j0 + g
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const double dg = __shfl_sync(0xFFFFFFFFu, sum, 4 * g);
+        const uint32_t j = j0 + g;
+        if (okg[g] && lane == (j & 31)) {
+          if (j & 32)
+            d[1] = dg;
+          else
+            d[0] = dg;
+        }
+      }
+    } else {
+      for (uint32_t g = 0; g < 8; ++g) {
+        const uint32_t j = j0 + g;
+        if (j >= K) break;
+        const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+        if (eo == kSentinel) continue;  // warp-uniform
+        const double dd = row_dist<NC>(vr, X, dp, eo);
+        if (lane == (j & 31)) {
+          if (j & 32)
+            d[1] = dd;
+          else
+            d[0] = dd;
+        }
+      }
+    }
+  }
   unsigned long long forced = 0, evict = 0;
   for (uint64_t r = b0; r < b1; ++r) {
     const uint32_t pq = s2p[(uint32_t)keys[r]];
-    int32_t free_pos = -1;
-    for (uint32_t c0 = 0; c0 < K && free_pos < 0; c0 += 32) {
-      uint32_t c = c0 + lane;
-      uint32_t fm = __ballot_sync(0xFFFFFFFFu, c < K && row[c] == kSentinel);
-      if (fm) free_pos = (int32_t)(c0 + __ffs(fm) - 1);
-    }
-    if (free_pos >= 0) {
-      __syncwarp();
-      if (lane == 0) row[free_pos] = pq;
+    const uint32_t f0 = __ballot_sync(0xFFFFFFFFu, e[0] == kSentinel && lane < K);
+    const uint32_t f1 = __ballot_sync(0xFFFFFFFFu, e[1] == kSentinel && lane + 32 < K);
+    int32_t pos;
+    if (f0 | f1) {
+      pos = f0 ? __ffs(f0) - 1 : 32 + __ffs(f1) - 1;
     } else {
-      const uint32_t r0 = K > k_local ? k_local : 0;
-      double best_st = -1.0, best_any = -1.0;
-      int32_t pos_st = -1, pos_any = -1;
-      for (uint32_t j = r0; j < K; ++j) {
-        const uint32_t e = row[j];
-        const double d = row_dist<NC>(vr, X, dp, e);
-        const uint32_t s = attr[e].slot;
-        if (d > best_any) {
-          best_any = d;
-          pos_any = (int32_t)j;
+      // first argmax over the region, stale entries first
+      int32_t best_pos = -1;
+      double best_d = kNegInf;
+      for (int pass = 0; pass < 2 && best_pos < 0; ++pass) {
+        double bd = kNegInf;
+        int32_t bp = 0x7FFFFFFF;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t j = lane + 32 * u;
+          const bool in = j >= r0 && j < K && (pass == 1 || st[u]);
+          if (in && (d[u] > bd || (d[u] == bd && (int32_t)j < bp))) {
+            bd = d[u];
+            bp = (int32_t)j;
+          }
         }
-        if ((s < start || s >= end) && d > best_st) {
-          best_st = d;
-          pos_st = (int32_t)j;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xFFFFFFFFu, bd, o);
+          const int32_t op = __shfl_xor_sync(0xFFFFFFFFu, bp, o);
+          if (od > bd || (od == bd && op < bp)) {
+            bd = od;
+            bp = op;
+          }
+        }
+        if (bp != 0x7FFFFFFF) {
+          best_pos = bp;
+          best_d = bd;
         }
       }
-      __syncwarp();
-      if (lane == 0) row[pos_st >= 0 ? pos_st : pos_any] = pq;
+      (void)best_d;
+      pos = best_pos;
       ++evict;
     }
+    const double dq = row_dist<NC>(vr, X, dp, pq);
+    if (lane == (uint32_t)(pos & 31)) {
+      const int u = pos >> 5;
+      if (u == 0) {
+        e[0] = pq;
+        d[0] = dq;
+        st[0] = false;
+      } else {
+        e[1] = pq;
+        d[1] = dq;
+        st[1] = false;
+      }
+    }
+    if (lane == 0) row[pos] = pq;
     __syncwarp();
     ++forced;
   }
