@@ -198,9 +198,28 @@ __global__ void k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const
     // nearest_kept[j] = min(nearest_kept[j], dist(s, cand j)) for the undecided tail
     RowRegs<NC> r;
     load_row<NC>(r, X, dp, s2p[s]);
-    for (uint32_t j = t + 1; j < n; ++j) {
-      double dj = row_dist<NC>(r, X, dp, s2p[cs[j]]);
-      if (lane == 0 && dj < near[j]) near[j] = dj;
+    if constexpr (NC == 1) {
+      // 8 candidate rows in flight per round; reduce_scatter is bit-identical to row_dist
+      const uint32_t col = lane * 4;
+      for (uint32_t j0 = t + 1; j0 < n; j0 += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const uint32_t j = j0 + g;
+          x[g] = (j < n && col < dp) ? ldg_nc_f4(X + (uint64_t)s2p[cs[j]] * dp + col) : make_float4(0, 0, 0, 0);
+        }
+        double part[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) part[g] = sq4(x[g], r.v[0], 0.0);
+        const double dsum = reduce_scatter<8>(part);  // lanes 4g .. 4g+3 hold candidate j0 + g
+        const uint32_t j = j0 + (lane >> 2);
+        if ((lane & 3) == 0 && j < n && dsum < near[j]) near[j] = dsum;
+      }
+    } else {
+      for (uint32_t j = t + 1; j < n; ++j) {
+        double dj = row_dist<NC>(r, X, dp, s2p[cs[j]]);
+        if (lane == 0 && dj < near[j]) near[j] = dj;
+      }
     }
     __syncwarp();
   }
