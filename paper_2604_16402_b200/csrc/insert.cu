@@ -255,7 +255,38 @@ __global__ void k_req_heads(const unsigned long long* keys, uint64_t n, uint8_t*
   head[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
 }
 
-// try_rewire for every request of one target v, in q order (updater.py:87-123)
+// Distances from the row in `r` to row entries j0 .. j0+7 of a lane-distributed
+// row (entry j held by lane j % 32 in e[j / 32]); entry j0 + g's distance is
+// returned on lanes 4g .. 4g+3 (SENTINEL / j >= K: +inf). d <= 128 only (NC = 1);
+// bit-identical to row_dist (reduce_scatter pairs like warp_sum).
+__device__ __forceinline__ double dist8(const RowRegs<1>& r, const float* X, uint32_t dp, const uint32_t (&e)[2],
+                                        uint32_t j0, uint32_t K) {
+  const uint32_t lane = lane_id(), col = lane * 4;
+  float4 x[8];
+  bool ok[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const uint32_t j = j0 + g;
+    const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+    ok[g] = j < K && eo != kSentinel;
+    x[g] = (ok[g] && col < dp) ? ldg_nc_f4(X + (uint64_t)eo * dp + col) : make_float4(0, 0, 0, 0);
+  }
+  double part[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) part[g] = sq4(x[g], r.v[0], 0.0);
+  const double sum = reduce_scatter<8>(part);
+  bool okl = false;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) okl = (lane >> 2) == (uint32_t)g ? ok[g] : okl;
+  return okl ? sum : __longlong_as_double(0x7FF0000000000000ll);
+}
+
+// try_rewire for every request of one target v, in q order (updater.py:87-123).
+// The row, and the distances from v to its eviction region, live in registers
+// (entry j on lane j % 32, e[j / 32]; K <= 64): a request reads no row memory,
+// the diversity test measures q against all K neighbours 8 rows per round
+// (stopping at the first failing round), and an accepted q's distance to v is
+// the request's own d_vq (the same f64 bits a recomputation gives).
 template <int NC>
 __global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint64_t nreq, const uint32_t* heads,
                          uint32_t nheads, const uint32_t* s2p, const Attr* attr, const float* X, uint32_t dp,
@@ -271,61 +302,115 @@ __global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint
   unsigned long long acc = 0, rej = 0, ev_nec = 0, ev_red = 0;
   RowRegs<NC> rv;
   load_row<NC>(rv, X, dp, pv);
+  const double kNegInf = -__longlong_as_double(0x7FF0000000000000ll);
+  const uint32_t r0 = K > k_local ? k_local : 0;
+  uint32_t e[2];
+  double dv[2] = {kNegInf, kNegInf};  // distance to v, region entries only
+  bool have_dv = false;                // computed lazily at the first eviction
+#pragma unroll
+  for (int u = 0; u < 2; ++u) e[u] = lane + 32 * u < K ? row[lane + 32 * u] : 0u;
   for (uint64_t r = b0; r < b1; ++r) {
     const uint32_t q = (uint32_t)keys[r];
     const uint32_t pq = s2p[q];
-    // duplicate?
-    bool dup = false, has_free = false;
-    int32_t free_pos = -1;
-    for (uint32_t c0 = 0; c0 < K; c0 += 32) {
-      uint32_t c = c0 + lane;
-      uint32_t e = c < K ? row[c] : 0u;
-      dup |= __any_sync(0xFFFFFFFFu, c < K && e == pq);
-      uint32_t fm = __ballot_sync(0xFFFFFFFFu, c < K && e == kSentinel);
-      if (fm && !has_free) {
-        has_free = true;
-        free_pos = (int32_t)(c0 + __ffs(fm) - 1);
-      }
-    }
-    if (dup) {
+    const bool in0 = lane < K, in1 = lane + 32 < K;
+    if (__any_sync(0xFFFFFFFFu, (in0 && e[0] == pq) || (in1 && e[1] == pq))) {  // duplicate
       ++rej;
       continue;
     }
-    if (has_free) {
-      __syncwarp();
-      if (lane == 0) row[free_pos] = pq;
-      __syncwarp();
-      ++acc;
-      continue;
-    }
-    // Eq.1/Eq.2 test against every current neighbour
-    const double deff = alpha2 * dvq[r];
-    RowRegs<NC> rq;
-    load_row<NC>(rq, X, dp, pq);
-    bool ok = true;
-    for (uint32_t j = 0; j < K && ok; ++j) ok = deff < row_dist<NC>(rq, X, dp, row[j]);
-    if (!ok) {
-      ++rej;
-      continue;
-    }
-    const uint32_t r0 = K > k_local ? k_local : 0;
-    double best = -1.0;
+    const uint32_t f0 = __ballot_sync(0xFFFFFFFFu, in0 && e[0] == kSentinel);
+    const uint32_t f1 = __ballot_sync(0xFFFFFFFFu, in1 && e[1] == kSentinel);
     int32_t pos = -1;
-    for (uint32_t j = r0; j < K; ++j) {
-      double dj = row_dist<NC>(rv, X, dp, row[j]);
-      if (dj > best) {
-        best = dj;
-        pos = (int32_t)j;
+    if (f0 | f1) {
+      pos = f0 ? __ffs(f0) - 1 : 32 + __ffs(f1) - 1;
+    } else {
+      // Eq.1/Eq.2 diversity test against every current neighbour
+      const double deff = alpha2 * dvq[r];
+      RowRegs<NC> rq;
+      load_row<NC>(rq, X, dp, pq);
+      bool ok = true;
+      if constexpr (NC == 1) {
+        for (uint32_t j0 = 0; j0 < K && ok; j0 += 8) {
+          const double dj = dist8(rq, X, dp, e, j0, K);
+          ok = !__any_sync(0xFFFFFFFFu, (lane & 3) == 0 && j0 + (lane >> 2) < K && !(deff < dj));
+        }
+      } else {
+        for (uint32_t j = 0; j < K && ok; ++j) {
+          const uint32_t ej = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+          ok = deff < row_dist<NC>(rq, X, dp, ej);
+        }
+      }
+      if (!ok) {
+        ++rej;
+        continue;
+      }
+      if (!have_dv) {
+        have_dv = true;
+        for (uint32_t j0 = r0; j0 < K; j0 += 8) {
+          if constexpr (NC == 1) {
+            const double dj = dist8(rv, X, dp, e, j0, K);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const double dg = __shfl_sync(0xFFFFFFFFu, dj, 4 * g);
+              const uint32_t j = j0 + g;
+              if (j < K && lane == (j & 31)) {
+                if (j & 32)
+                  dv[1] = dg;
+                else
+                  dv[0] = dg;
+              }
+            }
+          } else {
+            for (uint32_t j = j0; j < j0 + 8 && j < K; ++j) {
+              const uint32_t ej = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+              const double dg = row_dist<NC>(rv, X, dp, ej);
+              if (lane == (j & 31)) {
+                if (j & 32)
+                  dv[1] = dg;
+                else
+                  dv[0] = dg;
+              }
+            }
+          }
+        }
+      }
+      // farthest neighbour of v in the region, first index on ties
+      double bd = kNegInf;
+      int32_t bp = 0x7FFFFFFF;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t j = lane + 32 * u;
+        if (j >= r0 && j < K && (dv[u] > bd || (dv[u] == bd && (int32_t)j < bp))) {
+          bd = dv[u];
+          bp = (int32_t)j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(0xFFFFFFFFu, bd, o);
+        const int32_t op = __shfl_xor_sync(0xFFFFFFFFu, bp, o);
+        if (od > bd || (od == bd && op < bp)) {
+          bd = od;
+          bp = op;
+        }
+      }
+      pos = bp;
+      if ((uint32_t)pos >= k_local)
+        ++ev_red;
+      else
+        ++ev_nec;
+    }
+    if (lane == (uint32_t)(pos & 31)) {
+      if (pos & 32) {
+        e[1] = pq;
+        dv[1] = dvq[r];
+      } else {
+        e[0] = pq;
+        dv[0] = dvq[r];
       }
     }
-    __syncwarp();
     if (lane == 0) row[pos] = pq;
     __syncwarp();
     ++acc;
-    if ((uint32_t)pos >= k_local)
-      ++ev_red;
-    else
-      ++ev_nec;
   }
   if (lane == 0) {
     atomicAdd(&cnt->reverse_accepted, acc);
