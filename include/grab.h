@@ -196,6 +196,14 @@ GRAB_API int grab_try_rewire(const float* X, uint64_t n_rows, uint32_t dim, uint
                     uint32_t v, uint32_t q, double sq_dvq, double alpha, uint32_t k_local,
                     int32_t* accepted, int32_t* evicted_pos);
 
+/* ---- scc_count (evaluate.py:60-119): strongly connected components of the
+ * live graph (slot space; SENTINEL and targets >= live_count ignored), counted
+ * on the device (trim + forward-max coloring + backward closure). ---- */
+GRAB_API int grab_scc_count(const grab_index* h, uint64_t live_count, uint64_t* out);
+/* the same over an explicit slot-space adjacency (host pointer, rows x k_max) */
+GRAB_API int grab_scc_count_raw(const uint32_t* adjacency, uint64_t rows, uint32_t k_max, uint64_t live_count,
+                                uint64_t* out);
+
 /* ---- bucket-range sharded search (no reference counterpart:
  * the reference is single-process, so these replace nothing and follow the
  * reference's result convention -- ascending (distance, slot) with GLOBAL slot

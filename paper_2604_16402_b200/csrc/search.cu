@@ -621,7 +621,6 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           __syncwarp();
           // (2) drop SENTINEL / slot >= n, per-iteration unique, scalar pre-check
           uint32_t cand_bits = 0;
-#pragma unroll
           {
             // every first-probe CAS in flight before any is consumed; the table
             // (load <= 1/4) is left all-zero again by undoing this iteration's inserts
