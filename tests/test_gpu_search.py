@@ -119,3 +119,52 @@ def test_search_empty_index(g):
     gi = g.create_index(4, 16, g.BuildParams(k_max=4, k_local=2))
     r = g.search(gi, np.zeros(4, np.float32), g.SearchParams(k=3, itopk=8))
     assert len(r) == 0 and not r.truncated
+
+
+def _oracle_of(gi):
+    p = gi.params
+    n = gi.count
+    meta = gi.meta
+    return ist.OracleIndex(X=np.ascontiguousarray(gi.store.X[:n]), scalars=np.ascontiguousarray(gi.store.scalars[:n]),
+                           ids=np.arange(n), count=n, adjacency=np.ascontiguousarray(gi.adjacency[:n]),
+                           cfg=ist.BuildCfg(k_max=p.k_max, k_local=p.k_local, bucket_capacity=p.bucket_capacity),
+                           boundaries=meta.boundaries, i2b=meta.index_to_bucket[:n], b2i=meta.bucket_to_index)
+
+
+def test_wide_ranges_use_exact_hash_visited_set(g):
+    """Ranges whose slab interval exceeds the warp's bitmap (here > 131K rows at
+    itopk 64) switch the visited set to the open-addressing hash; results and
+    every SearchStats counter must still equal the oracle (searcher.py:156-233)."""
+    V, S = ist.gen_synthetic(300_000, 16, "gaussian", rng_seed=4)
+    gi, _ = g.build_index(V, S, g.BuildParams(k_max=16, k_local=8, bucket_capacity=3000))
+    ox = _oracle_of(gi)
+    Q, _ = ist.gen_synthetic(12, 16, "gaussian", rng_seed=5)
+    for lo, hi in ((-1.0, 2.0), (0.1, 0.8)):
+        p = g.SearchParams(k=10, itopk=64, search_width=4, max_iterations=50)
+        res = g.search_arrays(gi, Q, lo, hi, p, seed_base=3)
+        for i in range(len(Q)):
+            want = beam.beam_search(ox, Q[i], ist.SearchCfg(k=10, lower=lo, upper=hi, itopk=64, search_width=4,
+                                                            max_iterations=50, rng_seed=beam.derive_seed(3, i)))
+            c = int(res.counts[i])
+            assert np.array_equal(res.slots[i, :c], want.slots), (lo, i)
+            np.testing.assert_allclose(res.dists[i, :c], want.sq_dists, rtol=1e-12, atol=0)
+            got = [int(res.stats[i][f]) for f in STAT_KEYS]
+            ws = [getattr(want.stats, f) for f in STAT_KEYS]
+            assert got == ws, (lo, i, got, ws)
+
+
+def test_search_argument_errors_and_out_of_span(g, golden):
+    gold = golden("small")
+    gi = g.load_index(gold["container"].tobytes(), g.BuildParams(k_max=16, k_local=8, bucket_capacity=250))
+    q = np.zeros(8, np.float32)
+    with pytest.raises(ValueError):
+        g.search_arrays(gi, q, 0.5, 0.4, g.SearchParams(k=10, itopk=64))  # lower > upper
+    with pytest.raises(ValueError):
+        g.search_arrays(gi, q, 0.0, 1.0, g.SearchParams(k=10, itopk=64, search_width=16))  # width*K > 128
+    with pytest.raises(g.DimensionMismatchError):
+        g.search_arrays(gi, np.zeros(9, np.float32), 0.0, 1.0, g.SearchParams(k=10, itopk=64))
+    r = g.search_arrays(gi, np.stack([q, q]), np.array([5.0, -3.0]), np.array([6.0, -2.0]),
+                        g.SearchParams(k=10, itopk=64))
+    assert r.counts.tolist() == [0, 0] and (r.slots == -1).all()  # ranges outside the scalar span
+    s, d, c = g.brute_force_arrays(gi, np.stack([q, q]), np.array([5.0, -3.0]), np.array([6.0, -2.0]), 10)
+    assert c.tolist() == [0, 0]
