@@ -419,6 +419,13 @@ def main():
         g.search_arrays(gi, Qd, lod, hid, sp, seed_base=seed_base, stats=False)
         torch.cuda.synchronize()
         q = nq / (time.perf_counter() - t1)
+        if dist:  # every rank must pick the same operating point: global recall, slowest rank's QPS
+            t = torch.tensor([rec, -q], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            rec = float(t[0]) / world
+            t2 = torch.tensor([q], device=dev, dtype=torch.float64)
+            dist.all_reduce(t2, op=dist.ReduceOp.MIN)
+            q = float(t2[0])
         sweep.append({"itopk": itopk, "search_width": width, "max_iterations": iters, "recall": round(rec, 4),
                       "qps": round(q, 1)})
         if rec >= args.target and (point is None or q > point[3]):
