@@ -248,8 +248,7 @@ __device__ __forceinline__ uint64_t dc_key(float d, uint32_t col) {
 }
 
 // One descent round: one warp per node. Shared memory per warp: candidate ids
-// [C], their f32 distances [C] (first used as the "compute" flag) and an
-// H-entry id hash. First occurrences are found in column order: chunk by
+// [C], a compute-flag bitmask [C/32] and an H-entry id hash. First occurrences are found in column order: chunk by
 // chunk, the lowest lane of each id inside the chunk (match_any) inserts it,
 // and an id already present from an earlier chunk is a repeat.
 template <int WPB>
@@ -261,10 +260,11 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
   const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
   const uint32_t v = blockIdx.x * WPB + wib;
   if (v >= n) return;  // warp-uniform
-  uint8_t* base = smem + (size_t)wib * (C * 8 + H * 4);
+  const uint32_t NW = (C + 31) / 32;  // flag words
+  uint8_t* base = smem + (size_t)wib * (C * 4 + NW * 4 + H * 4);
   int32_t* cid = (int32_t*)base;
-  float* cd = (float*)(base + C * 4);
-  uint32_t* hkey = (uint32_t*)(base + C * 8);
+  uint32_t* fl = (uint32_t*)(base + C * 4);  // bit i of word w: compute column 32 w + i
+  uint32_t* hkey = fl + NW;
   const uint32_t J = 2 * k;
   const int32_t* jv = joint + (uint64_t)v * J;
   // (a) candidate ids: own joint row, then the joint rows of the hop sources
@@ -293,49 +293,54 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
         pend = cur != 0u && cur != (uint32_t)id + 1;
       }
     }
-    if (c < C) cd[c] = (lead && cur == 0u && (uint32_t)id != v) ? 0.0f : kInfF;  // 0 = compute
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, lead && cur == 0u && (uint32_t)id != v);
+    if (lane == 0) fl[b0 >> 5] = m;
   }
   __syncwarp();
-  // (c) distances of the first occurrences: 8-lane groups, 4 candidates per
-  // group per step (16 rows in flight per warp)
+  // (c) distances of the first occurrences and (d) the running top-k by
+  // (dist, column), 32 columns per chunk: 8-lane group g measures columns
+  // c0 + 8g + u (u = 0..7, 4 rows in flight at a time); after the group's
+  // xor-reduction lane 8g + s holds column c0 + 8g + s's distance in sums[s].
   const uint32_t pv = s2p[v];
   const float* qrow = X + (uint64_t)pv * dp;
   const uint32_t sub = lane & 7, grp = lane >> 3;
-  for (uint32_t b0 = 0; b0 < C; b0 += 16) {
-    uint32_t pc[4];
-    bool ok[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t c = b0 + grp * 4 + u;
-      ok[u] = c < C && cd[c] == 0.0f;
-      pc[u] = ok[u] ? s2p[cid[c]] : 0u;
-    }
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 2
-    for (uint32_t f = sub; f * 4 < dp; f += 8) {
-      const float4 q = *reinterpret_cast<const float4*>(qrow + 4 * f);
-      float4 x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = ok[u] ? ldg_nc_f4(X + (uint64_t)pc[u] * dp + 4 * f) : q;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = sq4(x[u], q, acc[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 4);
-      acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 2);
-      acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 1);
-      const uint32_t c = b0 + grp * 4 + u;
-      __syncwarp();
-      if (ok[u] && sub == 0) cd[c] = (float)acc[u];
-    }
-  }
-  __syncwarp();
-  // (d) top-k by (dist, column): running sorted list, one (key) per lane
   uint64_t best = ~0ull;  // lanes >= k never receive real entries
-  for (uint32_t b0 = 0; b0 < C; b0 += 32) {
-    const uint32_t c = b0 + lane;
-    uint64_t key = c < C ? dc_key(cd[c], c) : ~0ull;
+  for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+    const uint32_t flags = fl[c0 >> 5];
+    double sums[8];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t pc[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t bit = grp * 8 + half * 4 + u;
+        ok[u] = (flags >> bit) & 1u;
+        pc[u] = ok[u] ? s2p[cid[c0 + bit]] : 0u;
+      }
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+      for (uint32_t f = sub; f * 4 < dp; f += 8) {
+        const float4 q = *reinterpret_cast<const float4*>(qrow + 4 * f);
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = ok[u] ? ldg_nc_f4(X + (uint64_t)pc[u] * dp + 4 * f) : q;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = sq4(x[u], q, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 4);
+        acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 2);
+        acc[u] += __shfl_xor_sync(0xFFFFFFFFu, acc[u], 1);
+        sums[half * 4 + u] = acc[u];
+      }
+    }
+    double mine = sums[0];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) mine = sub == (uint32_t)u ? sums[u] : mine;
+    const uint32_t c = c0 + lane;
+    uint64_t key = c < C ? dc_key(((flags >> lane) & 1u) ? (float)mine : kInfF, c) : ~0ull;
     const uint64_t tail = __shfl_sync(0xFFFFFFFFu, best, k - 1);
     if (!__any_sync(0xFFFFFFFFu, key < tail)) continue;
     // sort the chunk ascending
@@ -476,8 +481,8 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   uint32_t* dhop = S.alloc<uint32_t>(J);
   int end_bit = 1;
   while ((1ull << end_bit) <= n) ++end_bit;
-  constexpr int WPB = 4;
-  const size_t smem = (size_t)WPB * (C * 8 + H * 4);
+  constexpr int WPB = 1;
+  const size_t smem = (size_t)WPB * (C * 4 + (C + 31) / 32 * 4 + H * 4);
   GRAB_CUDA(cudaFuncSetAttribute(k_descent<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (uint32_t r = 0; r < rounds; ++r) {
     // reverse top-k: stable sort by (dist, src), then by dst
