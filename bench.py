@@ -519,7 +519,7 @@ def main():
 
     # ---- insert vectors/s: one append-only batch into the built index (N_cap = 2n)
     ins_b = min(args.insert_batch, gi.capacity - gi.count)
-    Xi, Si = ds.gen_lowrank(ins_b, dim, seed=2)
+    Xi, Si = ds.gen_lowrank(ins_b, dim, seed=2, w_seed=0)  # in-distribution new rows (same basis)
     Xi_d = torch.from_numpy(Xi).to(dev)
     Si_d = torch.from_numpy(Si).to(dev)
     torch.cuda.synchronize()

@@ -416,7 +416,7 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
                         reverse_accepted=int(rep.reverse_accepted), reverse_rejected=int(rep.reverse_rejected),
                         evictions_necessary=int(rep.evictions_necessary),
                         evictions_redundant=int(rep.evictions_redundant), forced_links=int(rep.forced_links),
-                        rewired_rows=[int(x) for x in rw], wall_time_s=float(rep.wall_time_s),
+                        rewired_rows=rw.astype(np.int64).tolist(), wall_time_s=float(rep.wall_time_s),
                         phase_seconds={k: float(rep.phase_seconds[i]) for i, k in enumerate(_INSERT_PHASES)})
 
 

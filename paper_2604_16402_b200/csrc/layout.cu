@@ -250,7 +250,9 @@ static void relayout(DevIndex& ix, const std::vector<uint32_t>& extra) {
   for (uint32_t b = 0; b < m; ++b) {
     nstart[b] = (uint32_t)total;
     uint64_t want = (uint64_t)ix.h_bcount[b] + extra[b];
-    ncap[b] = std::max(ix.h_bcap[b], slab_cap(want + want / 8));
+    // geometric growth: a relayout leaves 50 % headroom so append-only batches
+    // relayout O(log) times, not once per batch
+    ncap[b] = std::max(ix.h_bcap[b], slab_cap(want + want / 2));
     total += ncap[b];
   }
   if (total >= 0xFFFFFFFFull) throw Error(GRAB_ERR_CAPACITY, "physical rows exceed u32 id space");

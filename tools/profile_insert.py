@@ -11,7 +11,7 @@ b = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
 X, S = ds.gen_lowrank(n, 128, seed=0)
 gi, rep = g.build_index(X, S, g.BuildParams(k_max=32, k_local=16, bucket_capacity=10_000))
 print("build", rep.to_dict() | {"bucket_sizes": None})
-Xi, Si = ds.gen_lowrank(b, 128, seed=2)
+Xi, Si = ds.gen_lowrank(b, 128, seed=2, w_seed=0)
 r = g.insert_batch(gi, Xi, Si)
 d = r.to_dict()
 d.pop("rewired_rows")
