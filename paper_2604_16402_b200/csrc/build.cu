@@ -560,7 +560,8 @@ uint32_t reinforce_device(DevIndex& ix, const uint32_t* rows, uint64_t n, cudaSt
     if (no == 0) break;
     // ascending slot order (np.flatnonzero), then to phys
     std::vector<uint32_t> h(no);
-    GRAB_CUDA(cudaMemcpy(h.data(), list, no * 4, cudaMemcpyDeviceToHost));
+    GRAB_CUDA(cudaMemcpyAsync(h.data(), list, no * 4, cudaMemcpyDeviceToHost, st));
+    GRAB_CUDA(cudaStreamSynchronize(st));
     std::sort(h.begin(), h.end());
     GRAB_CUDA(cudaMemcpyAsync(list, h.data(), no * 4, cudaMemcpyHostToDevice, st));
     k_slots_to_phys<<<(unsigned)div_up(no, 256), 256, 0, st>>>(list, no, ix.slot2phys);

@@ -159,9 +159,13 @@ static void place_batch(DevIndex& ix, const float* Xsrc, const float* Ssrc, uint
   uint32_t* sorted = sort_slots_by_bucket(ix, start, n);
   // per-bucket counts within the batch -> first position of each bucket
   std::vector<int32_t> hb(n);
-  GRAB_CUDA(cudaMemcpy(hb.data(), ix.i2b + start, n * 4, cudaMemcpyDeviceToHost));
+  GRAB_CUDA(cudaMemcpyAsync(hb.data(), ix.i2b + start, n * 4, cudaMemcpyDeviceToHost, ix.stream));
+  GRAB_CUDA(cudaStreamSynchronize(ix.stream));
   std::vector<uint64_t> first(ix.m + 1, 0);
-  for (uint64_t i = 0; i < n; ++i) first[hb[i] + 1]++;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (hb[i] < 0 || (uint32_t)hb[i] >= ix.m) throw Error(GRAB_ERR_CUDA, "place: bucket id out of range");
+    first[hb[i] + 1]++;
+  }
   for (uint32_t b = 0; b < ix.m; ++b) first[b + 1] += first[b];
   uint32_t* d_base;
   uint64_t* d_first;
@@ -298,9 +302,16 @@ static void relayout(DevIndex& ix, const std::vector<uint32_t>& extra) {
 
 void layout_append(DevIndex& ix, const float* X_new, const float* S_new, uint64_t start, uint64_t b) {
   std::vector<int32_t> hb(b);
-  GRAB_CUDA(cudaMemcpy(hb.data(), ix.i2b + start, b * 4, cudaMemcpyDeviceToHost));
+  // the bucket ids were computed on ix.stream (non-blocking): read them on that
+  // stream -- a legacy-stream cudaMemcpy does not wait for it and could see the
+  // -1 fill, indexing `extra` out of bounds
+  GRAB_CUDA(cudaMemcpyAsync(hb.data(), ix.i2b + start, b * 4, cudaMemcpyDeviceToHost, ix.stream));
+  GRAB_CUDA(cudaStreamSynchronize(ix.stream));
   std::vector<uint32_t> extra(ix.m, 0);
-  for (uint64_t i = 0; i < b; ++i) extra[hb[i]]++;
+  for (uint64_t i = 0; i < b; ++i) {
+    if (hb[i] < 0 || (uint32_t)hb[i] >= ix.m) throw Error(GRAB_ERR_CUDA, "append: bucket id out of range");
+    extra[hb[i]]++;
+  }
   bool overflow = false;
   for (uint32_t k = 0; k < ix.m; ++k)
     if ((uint64_t)ix.h_bcount[k] + extra[k] > ix.h_bcap[k]) overflow = true;
