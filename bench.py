@@ -197,6 +197,19 @@ def _timed(fn, stream):
     return e0.elapsed_time(e1), out
 
 
+def _gpu_warm(device: int, seconds: float = 0.5):
+    """Keep the GPU busy (bf16 matmuls) for `seconds` so clocks are up before a
+    one-shot measurement."""
+    import torch
+    a = torch.randn(4096, 4096, device=f"cuda:{device}", dtype=torch.bfloat16)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(20):
+            a = (a @ a).clamp_(-1, 1)
+        torch.cuda.synchronize()
+    del a
+
+
 def _max_over_ranks(v, dist, dev):
     if not dist:
         return v
@@ -221,6 +234,7 @@ def run_dynamic(args, cfg, rank, world, local, dist):
     total, batch = args.inserts or cfg["inserts"], cfg["batch"]
     X, S = ds.gen_lowrank(n + total, dim, seed=0)
     params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
+    _gpu_warm(local)
     t0 = time.perf_counter()
     gi, brep = g.build_index(X[:n], S[:n], params, capacity=n + total, device=local, global_pass=args.global_pass)
     torch.cuda.synchronize()
@@ -288,6 +302,7 @@ def run_sharded(args, cfg, rank, world, local, dist):
     gid = np.arange(n, dtype=np.int64) + rank * n
     # the paper's scale setting: M = K_max = 64, global pool k_g = 32
     params = g.BuildParams(k_max=64, k_local=32, bucket_capacity=cap)
+    _gpu_warm(local)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     idx, brep = sh.ShardedIndex.build(X, S, gid, params, rank=rank, world=world, device=local,
@@ -394,7 +409,10 @@ def main():
     Q, lo, hi = Qall[sl], lo_all[sl], hi_all[sl]
     params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
 
-    # ---- build (replicated per rank; deterministic)
+    # ---- build (replicated per rank; deterministic). A fresh process starts on an
+    # idle GPU whose clocks ramp over the first ~0.5 s of work; spin the GPU for a
+    # moment first so build_s measures the build, not the clock ramp.
+    _gpu_warm(local)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     gi, brep = g.build_index(X, S, params, device=local, global_pass=args.global_pass)
