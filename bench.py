@@ -306,7 +306,8 @@ def run_sharded(args, cfg, rank, world, local, dist):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     idx, brep = sh.ShardedIndex.build(X, S, gid, params, rank=rank, world=world, device=local,
-                                      global_pass=args.global_pass, refine_rounds=args.refine_rounds or 10, k_g=32)
+                                      global_pass=args.global_pass, refine_rounds=args.refine_rounds or 10, k_g=32,
+                                      exchange=args.exchange)
     torch.cuda.synchronize()
     build_s = _max_over_ranks(time.perf_counter() - t0, dist, dev)
     del X
@@ -345,7 +346,8 @@ def run_sharded(args, cfg, rank, world, local, dist):
                                    f"width 2 / 200 it, NN-descent rounds {args.refine_rounds or 10}",
                        "rows_per_gpu": n, "queries": NQ, "recall_at_10": round(rec, 4),
                        "routed_queries_rank0": int(res.routed), "index": "bucket-range sharded",
-                       "exchange": "NCCL all_to_all_single" if dist else "none (1 shard)",
+                       "exchange": ("peer-memory stores (CUDA IPC over NVLink)" if args.exchange == "p2p"
+                                    else "NCCL all_to_all_single") if dist else "none (1 shard)",
                        "global_pass": brep.global_pass},
             "build_s": round(build_s, 3), "gpu_launches": None, "clocks": clk.summary()}
     if rank == 0:
@@ -372,6 +374,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--insert-batch", type=int, default=100_000)
     ap.add_argument("--inserts", type=int, help="cfg4: rows inserted after the build")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="cfg5: fused peer-memory stores (p2p) or NCCL all-to-all of staged blocks")
     ap.add_argument("--itopk", type=int, help="operating point of the cfg4 / cfg5 modes (320 / 512)")
     ap.add_argument("--refine-rounds", type=int, help="NN-descent rounds (reference default 3; cfg5 uses 10)")
     ap.add_argument("--global-pass", default="auto", choices=["auto", "exact", "descent"],

@@ -214,6 +214,20 @@ GRAB_API int grab_scc_count_raw(const uint32_t* adjacency, uint64_t rows, uint32
 GRAB_API int grab_shard_pack(uint64_t n, const uint32_t* qidx, const int64_t* slots, const double* dists,
                              const int64_t* gid, uint32_t k, uint32_t world, uint32_t B, double* send_d,
                              int64_t* send_i, void* stream);
+/* Fused exchange over peer memory (NVLink): pack straight into every owner's
+ * receive buffer [src][B][k] through CUDA IPC mappings. peer_d / peer_i are
+ * device arrays of `world` pointers (entry r = rank r's receive buffer, the
+ * local one for r == rank); this rank fills its slice [rank] of every owner's
+ * buffer with NaN / -1, then stores its results. The caller synchronizes the
+ * ranks (stream sync + barrier) before grab_merge_topk. */
+GRAB_API int grab_shard_pack_p2p(uint64_t n, const uint32_t* qidx, const int64_t* slots, const double* dists,
+                                 const int64_t* gid, uint32_t k, uint32_t rank, uint32_t world, uint32_t B,
+                                 double* const* peer_d, int64_t* const* peer_i, void* stream);
+/* IPC-shareable device buffers: allocate (64-byte handle out), open a peer's, close, free */
+GRAB_API int grab_ipc_alloc(uint64_t bytes, void** ptr, void* handle64);
+GRAB_API int grab_ipc_open(const void* handle64, void** ptr);
+GRAB_API int grab_ipc_close(void* ptr);
+GRAB_API int grab_ipc_free(void* ptr);
 /* derive_query_seed(base, ordinals[i]) for a routed subset of a batch
  * (searcher.py:85-87; host pointers) */
 GRAB_API int grab_derive_seeds(uint64_t base, const uint32_t* ordinals, uint64_t n, uint64_t* out);

@@ -95,6 +95,11 @@ _SIGS = {
     "grab_try_rewire": (C.c_int, [P, u64, u32, P, u32, u32, u32, dbl, dbl, u32, P, P]),
     "grab_shard_pack": (C.c_int, [u64, P, P, P, P, u32, u32, u32, P, P, P]),
     "grab_merge_topk": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, P]),
+    "grab_shard_pack_p2p": (C.c_int, [u64, P, P, P, P, u32, u32, u32, u32, P, P, P]),
+    "grab_ipc_alloc": (C.c_int, [u64, C.POINTER(P), P]),
+    "grab_ipc_open": (C.c_int, [P, C.POINTER(P)]),
+    "grab_ipc_close": (C.c_int, [P]),
+    "grab_ipc_free": (C.c_int, [P]),
     "grab_derive_seeds": (C.c_int, [u64, P, u64, P]),
     "grab_scc_count": (C.c_int, [P, u64, P]),
     "grab_scc_count_raw": (C.c_int, [P, u64, u32, u64, P]),

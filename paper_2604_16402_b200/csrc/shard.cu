@@ -8,6 +8,8 @@
 // one fixed-size all-to-all (NCCL over NVLink), and each owner merges the
 // world x k candidates of its queries by (distance, global slot), the
 // reference's tie rule (searcher.py:64-71).
+#include <cstring>
+
 #include "index.cuh"
 
 namespace grab {
@@ -101,6 +103,97 @@ extern "C" GRAB_API int grab_merge_topk(uint32_t nq, uint32_t nsrc, uint32_t B, 
     if (nq) {
       k_merge_topk<<<(unsigned)div_up(nq, 128), 128, 0, (cudaStream_t)stream>>>(nq, nsrc, B, k, d, id, out_d, out_i,
                                                                                 out_c);
+      GRAB_CHECK_LAUNCH();
+    }
+    return GRAB_OK;
+  } catch (const Error& e) {
+    return grab_set_error(e.code, e.what());
+  }
+}
+
+// ---------------------------------------------------------------- peer-memory exchange
+// The fused variant of pack + all-to-all: every rank stores its per-query
+// top-k straight into the OWNER rank's receive buffer over NVLink (CUDA IPC
+// mappings of the peers' buffers), so the exchange is the search epilogue's own
+// stores -- no staging buffer, no collective kernel. recv layout on every rank:
+// [src rank][B][k]; rank r writes only slice [r] of each owner's buffer.
+namespace grab {
+
+__global__ void k_shard_fill_p2p(uint64_t total, uint32_t rank, uint32_t B, uint32_t k, uint32_t world,
+                                 double* const* peer_d, int64_t* const* peer_i) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= total) return;  // total = world * B * k
+  const uint32_t owner = (uint32_t)(t / ((uint64_t)B * k));
+  const uint64_t within = t % ((uint64_t)B * k);
+  const uint64_t off = (uint64_t)rank * B * k + within;
+  peer_d[owner][off] = __longlong_as_double(0x7FF8000000000000ll);
+  peer_i[owner][off] = -1;
+}
+
+__global__ void k_shard_pack_p2p(uint64_t n, const uint32_t* __restrict__ qidx, const int64_t* __restrict__ slots,
+                                 const double* __restrict__ dists, const int64_t* __restrict__ gid, uint32_t k,
+                                 uint32_t rank, uint32_t B, double* const* peer_d, int64_t* const* peer_i) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= n * k) return;
+  const uint64_t i = t / k, j = t % k;
+  const uint32_t q = qidx[i];
+  const uint32_t owner = q / B;
+  const uint64_t off = ((uint64_t)rank * B + q % B) * k + j;
+  const int64_t s = slots[i * k + j];
+  peer_d[owner][off] = s >= 0 ? dists[i * k + j] : __longlong_as_double(0x7FF8000000000000ll);
+  peer_i[owner][off] = s >= 0 ? gid[s] : -1;
+  if (t == n * k - 1) __threadfence_system();
+}
+
+}  // namespace grab
+
+extern "C" GRAB_API int grab_ipc_alloc(uint64_t bytes, void** ptr, void* handle64) {
+  try {
+    GRAB_CUDA(cudaMalloc(ptr, bytes ? bytes : 16));
+    cudaIpcMemHandle_t h;
+    GRAB_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+    return GRAB_OK;
+  } catch (const Error& e) {
+    return grab_set_error(e.code, e.what());
+  }
+}
+
+extern "C" GRAB_API int grab_ipc_open(const void* handle64, void** ptr) {
+  try {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    GRAB_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return GRAB_OK;
+  } catch (const Error& e) {
+    return grab_set_error(e.code, e.what());
+  }
+}
+
+extern "C" GRAB_API int grab_ipc_close(void* ptr) {
+  cudaIpcCloseMemHandle(ptr);
+  return GRAB_OK;
+}
+
+extern "C" GRAB_API int grab_ipc_free(void* ptr) {
+  cudaFree(ptr);
+  return GRAB_OK;
+}
+
+extern "C" GRAB_API int grab_shard_pack_p2p(uint64_t n, const uint32_t* qidx, const int64_t* slots,
+                                            const double* dists, const int64_t* gid, uint32_t k, uint32_t rank,
+                                            uint32_t world, uint32_t B, double* const* peer_d, int64_t* const* peer_i,
+                                            void* stream) {
+  try {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (k == 0 || world == 0 || B == 0 || rank >= world) throw Error(GRAB_ERR_VALUE, "bad shard geometry");
+    const uint64_t total = (uint64_t)world * B * k;
+    k_shard_fill_p2p<<<(unsigned)div_up(total, 256), 256, 0, st>>>(total, rank, B, k, world, peer_d, peer_i);
+    GRAB_CHECK_LAUNCH();
+    if (n) {
+      k_shard_pack_p2p<<<(unsigned)div_up(n * k, 256), 256, 0, st>>>(n, qidx, slots, dists, gid, k, rank, B, peer_d,
+                                                                     peer_i);
       GRAB_CHECK_LAUNCH();
     }
     return GRAB_OK;

@@ -15,7 +15,9 @@ unchanged single-GPU pipeline. A query batch is served by:
 3. ``grab_shard_pack``: local slots -> global ids, written into the block of the
    rank that owns the query (owner = i // B, B = ceil(nq / world));
 4. one fixed-size all-to-all of those blocks (NCCL over NVLink on GPUs, gloo in
-   the CPU tests);
+   the CPU tests) -- or, with ``exchange="p2p"``, no collective at all: the pack
+   kernel stores straight into each owner's receive buffer through CUDA IPC
+   mappings (NVLink peer memory), bracketed by two barriers;
 5. ``grab_merge_topk``: each owner merges world x k candidates per query by
    (distance, global id), the reference's tie rule.
 
@@ -26,6 +28,7 @@ brute-force kernel in step 2).
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 
@@ -92,12 +95,64 @@ class ShardResult:
 class ShardedIndex:
     """One rank's shard plus the group-wide routing table."""
 
-    def __init__(self, local, gid, spans: np.ndarray, rank: int, world: int, group=None, device: int = 0):
+    def __init__(self, local, gid, spans: np.ndarray, rank: int, world: int, group=None, device: int = 0,
+                 exchange: str = "nccl"):
         import torch
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"unknown exchange: {exchange!r}")
         self.local = local
         self.rank, self.world, self.group, self.device = rank, world, group, device
+        self.exchange = exchange
         self.spans = np.asarray(spans, dtype=np.float32)
         self.gid = torch.as_tensor(np.ascontiguousarray(gid, dtype=np.int64), device=self._dev())
+        self._peers = None  # (B, k) -> peer receive buffers for exchange="p2p"
+
+    def _peer_buffers(self, B: int, k: int):
+        """Receive buffers [world][B][k] (dists, ids) on every rank, mapped into
+        every other rank through CUDA IPC (allocated once per (B, k))."""
+        import torch
+        import torch.distributed as dist
+        if self._peers is not None and self._peers["shape"] == (B, k):
+            return self._peers
+        self.close_peers()
+        nbytes = self.world * B * k * 8
+        own, handles = [], []
+        for _ in range(2):
+            p = C.c_void_p()
+            h = (C.c_uint8 * 64)()
+            L.check(L.lib.grab_ipc_alloc(nbytes, C.byref(p), h))
+            own.append(p.value)
+            handles.append(bytes(h))
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, handles, group=self.group)
+        else:
+            allh = [handles]
+        ptrs, opened = [[0] * self.world, [0] * self.world], []
+        for r in range(self.world):
+            for t in range(2):
+                if r == self.rank:
+                    ptrs[t][r] = own[t]
+                else:
+                    p = C.c_void_p()
+                    hb = (C.c_uint8 * 64).from_buffer_copy(allh[r][t])
+                    L.check(L.lib.grab_ipc_open(hb, C.byref(p)))
+                    ptrs[t][r] = p.value
+                    opened.append(p.value)
+        dev = self._dev()
+        self._peers = {"shape": (B, k), "own": own, "opened": opened,
+                       "ptr_d": torch.tensor(ptrs[0], dtype=torch.int64, device=dev),
+                       "ptr_i": torch.tensor(ptrs[1], dtype=torch.int64, device=dev)}
+        return self._peers
+
+    def close_peers(self) -> None:
+        if self._peers is None:
+            return
+        for p in self._peers["opened"]:
+            L.lib.grab_ipc_close(C.c_void_p(p))
+        for p in self._peers["own"]:
+            L.lib.grab_ipc_free(C.c_void_p(p))
+        self._peers = None
 
     def _dev(self):
         import torch
@@ -106,7 +161,7 @@ class ShardedIndex:
     # ------------------------------------------------------------------ build
     @classmethod
     def build(cls, X_local, S_local, gid_local, params: BuildParams, *, rank: int, world: int, group=None,
-              device: int = 0, **build_kw):
+              device: int = 0, exchange: str = "nccl", **build_kw):
         """Build this rank's shard from its own rows (already restricted to its
         scalar range) and exchange the shard spans."""
         import torch
@@ -121,7 +176,7 @@ class ShardedIndex:
             spans = torch.cat(parts).cpu().numpy()
         else:
             spans = mine
-        return cls(local, gid_local, spans, rank, world, group, device), report
+        return cls(local, gid_local, spans, rank, world, group, device, exchange), report
 
     # ------------------------------------------------------------------ query
     def search(self, queries, lower, upper, params: SearchParams, *, seed_base: int | None = None,
@@ -153,19 +208,36 @@ class ShardedIndex:
             base = params.rng_seed if seed_base is None else seed_base
             r = search_arrays(self.local, Qm, lo_m, hi_m, params, seeds=derive_seeds(base, mine), stats=False)
             slots, dists = r.slots, r.dists
-        send_d = torch.empty((self.world, B, k), dtype=torch.float64, device=dev)
-        send_i = torch.empty((self.world, B, k), dtype=torch.int64, device=dev)
         qidx = torch.from_numpy(mine).to(dev)
         stream = torch.cuda.current_stream(dev).cuda_stream
-        L.check(L.lib.grab_shard_pack(len(mine), L.ptr(qidx), L.ptr(slots.contiguous()), L.ptr(dists.contiguous()),
-                                      L.ptr(self.gid), k, self.world, B, L.ptr(send_d), L.ptr(send_i), stream))
-        recv_d, recv_i = exchange(send_d, send_i, self.world, self.group, self.device)
+        if self.exchange == "p2p":
+            # fused exchange: stores straight into the owners' receive buffers over NVLink
+            import torch.distributed as dist
+            pb = self._peer_buffers(B, k)
+            if self.world > 1:
+                dist.barrier(group=self.group)  # owners are done merging the previous batch
+            L.check(L.lib.grab_shard_pack_p2p(len(mine), L.ptr(qidx), L.ptr(slots.contiguous()),
+                                              L.ptr(dists.contiguous()), L.ptr(self.gid), k, self.rank, self.world, B,
+                                              L.ptr(pb["ptr_d"]), L.ptr(pb["ptr_i"]), stream))
+            if self.world > 1:
+                torch.cuda.current_stream(dev).synchronize()
+                dist.barrier(group=self.group)  # every rank's stores have landed
+            recv_d, recv_i = C.c_void_p(pb["own"][0]), C.c_void_p(pb["own"][1])
+        else:
+            send_d = torch.empty((self.world, B, k), dtype=torch.float64, device=dev)
+            send_i = torch.empty((self.world, B, k), dtype=torch.int64, device=dev)
+            L.check(L.lib.grab_shard_pack(len(mine), L.ptr(qidx), L.ptr(slots.contiguous()),
+                                          L.ptr(dists.contiguous()), L.ptr(self.gid), k, self.world, B,
+                                          L.ptr(send_d), L.ptr(send_i), stream))
+            recv_d, recv_i = exchange(send_d, send_i, self.world, self.group, self.device)
         first = self.rank * B
         n_own = max(0, min(B, nq - first))
         out_d = torch.empty((n_own, k), dtype=torch.float64, device=dev)
         out_i = torch.empty((n_own, k), dtype=torch.int64, device=dev)
         out_c = torch.empty(n_own, dtype=torch.int32, device=dev)
-        L.check(L.lib.grab_merge_topk(n_own, self.world, B, k, L.ptr(recv_d), L.ptr(recv_i), L.ptr(out_d),
+        rd = recv_d if isinstance(recv_d, C.c_void_p) else L.ptr(recv_d)
+        ri = recv_i if isinstance(recv_i, C.c_void_p) else L.ptr(recv_i)
+        L.check(L.lib.grab_merge_topk(n_own, self.world, B, k, rd, ri, L.ptr(out_d),
                                       L.ptr(out_i), L.ptr(out_c), torch.cuda.current_stream(dev).cuda_stream))
         return ShardResult(first, out_i, out_d, out_c, len(mine))
 

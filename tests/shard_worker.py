@@ -3,11 +3,13 @@ tests/test_shard.py): spawns `world` ranks on 127.0.0.1 with the gloo backend.
 
   --mode exchange   CPU only: plan / route / pack-layout / all-to-all / merge
                     semantics checked against the numpy restatements.
-  --mode gpu        every rank shares cuda:0: builds its shard with libgrab,
+  --mode gpu[_p2p]  every rank shares cuda:0: builds its shard with libgrab,
                     serves a query batch through route -> search -> pack ->
                     all-to-all -> merge, and rank 0 checks the merged exact
                     pipeline against the single-index brute force (bit-exact
-                    ids) and the search recall against it.
+                    ids) and the search recall against it. gpu_p2p runs the
+                    fused exchange: IPC-mapped receive buffers written by
+                    the pack kernel of every rank.
 """
 from __future__ import annotations
 
@@ -72,7 +74,7 @@ def run_exchange(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def run_gpu(rank, world, port, out):
+def run_gpu(rank, world, port, out, exchange="nccl"):
     import numpy as np
     import torch
 
@@ -90,7 +92,7 @@ def run_gpu(rank, world, port, out):
     owner = sh.shard_of(S, cuts)
     gid = np.nonzero(owner == rank)[0]
     params = g.BuildParams(k_max=16, k_local=8, bucket_capacity=500)
-    idx, _ = sh.ShardedIndex.build(X[gid], S[gid], gid, params, rank=rank, world=world, device=0)
+    idx, _ = sh.ShardedIndex.build(X[gid], S[gid], gid, params, rank=rank, world=world, device=0, exchange=exchange)
     sp = g.SearchParams(k=k, itopk=64)
     ex = idx.search(Q, lo, hi, sp, exact=True)
     se = idx.search(Q, lo, hi, sp, seed_base=0)
@@ -115,15 +117,19 @@ def run_gpu(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def run_gpu_p2p(rank, world, port, out):
+    run_gpu(rank, world, port, out, exchange="p2p")
+
+
 def main():
     import torch.multiprocessing as mp
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", choices=["exchange", "gpu"], required=True)
+    ap.add_argument("--mode", choices=["exchange", "gpu", "gpu_p2p"], required=True)
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--port", type=int, default=29533)
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
-    fn = run_exchange if a.mode == "exchange" else run_gpu
+    fn = {"exchange": run_exchange, "gpu": run_gpu, "gpu_p2p": run_gpu_p2p}[a.mode]
     mp.spawn(fn, args=(a.world, a.port, a.out), nprocs=a.world)
 
 

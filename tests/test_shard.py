@@ -83,3 +83,12 @@ def test_sharded_pipeline_world2_on_one_gpu(tmp_path):
     assert res["exact_ok"], res  # sharded exact pipeline == single-index brute force, id for id
     assert res["recall"] >= 0.9, res
     assert res["routed"] > 0
+
+
+@pytest.mark.gpu
+def test_sharded_pipeline_p2p_exchange_world2_on_one_gpu(tmp_path):
+    """The fused exchange: each rank's pack kernel stores into the owner's
+    CUDA-IPC-mapped receive buffer (two processes on one device); same results."""
+    res = _run("gpu_p2p", 2, 29545, tmp_path, 600)
+    assert res["exact_ok"], res
+    assert res["recall"] >= 0.9, res
