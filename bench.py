@@ -164,15 +164,17 @@ def oracle_index_from(gi):
     return idx
 
 
-def cpu_search_qps(idx, Q, lo, hi, seeds, point, procs: int, steps: int):
-    """Times the oracle port: `steps` repetitions over the sample, fork pool of `procs`."""
+def cpu_search_qps(idx, Q, lo, hi, seeds, point, procs: int, steps: int, warmup: int = 1):
+    """Times the oracle port: `warmup` untimed then `steps` timed passes over the
+    sample, fork pool of `procs`."""
     import multiprocessing as mp
     _CPU["idx"] = idx
     items = [(i, Q[i], float(lo[i]), float(hi[i]), int(seeds[i]), point) for i in range(len(Q))]
     chunks = [items[i::procs] for i in range(procs)]
     ctx = mp.get_context("fork")
     with ctx.Pool(procs) as pool:
-        pool.map(_cpu_worker, [c[:2] for c in chunks])  # warm the workers
+        for _ in range(max(warmup, 1)):
+            pool.map(_cpu_worker, chunks)
         t0 = time.perf_counter()
         for _ in range(steps):
             res = pool.map(_cpu_worker, chunks)
@@ -469,16 +471,20 @@ def main():
     if args.impl == "reference":
         procs = os.cpu_count() or 1
         idx = oracle_index_from(gi)
-        m = min(args.cpu_sample, nq)
+        # each step = one pass over a bounded sample (8 queries per host core)
+        m = min(8 * procs, nq)
         seeds = [int(np.random.SeedSequence([seed_base, i]).generate_state(1, np.uint64)[0]) for i in range(m)]
-        steps = max(1, args.steps // 10)
-        qps, el, _ = cpu_search_qps(idx, Q[:m], lo[:m], hi[:m], seeds, (itopk, width, iters), procs, steps)
+        steps = args.steps
+        qps, el, _ = cpu_search_qps(idx, Q[:m], lo[:m], hi[:m], seeds, (itopk, width, iters), procs, steps,
+                                    args.warmup)
         line = {"impl": "reference", "metric": "range-filtered QPS @ recall@10=0.95", "value": round(qps, 2),
-                "unit": "queries/s", "n_gpus": 1, "steps": steps, "warmup": 1, "ms_per_step": el / steps * 1e3,
+                "unit": "queries/s", "n_gpus": 1, "steps": steps, "warmup": args.warmup,
+                "ms_per_step": el / steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": round(qps, 2), "unit": "queries/s", "cores": procs, "kind": "port",
-                                 "sample": f"{m} queries x {steps} passes of the numpy port of searcher.py (oracle/beam.py) "
+                                 "sample": f"{m} of the {nq} queries per step x {steps} steps of the numpy port of "
+                                           f"searcher.py (oracle/beam.py) "
                                            f"on the same graph (built on the GPU, exported to slot layout), fork pool of {procs}"},
                 "e2e": {"value": round(qps, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
