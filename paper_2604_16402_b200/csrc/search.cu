@@ -621,7 +621,16 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           __syncwarp();
           // (2) drop SENTINEL / slot >= n, per-iteration unique, scalar pre-check
           uint32_t cand_bits = 0;
-          {
+          if (!a.out_stats) {
+            // no SearchStats requested: the per-iteration unique only feeds the
+            // `gathered` / `precheck_rejected` counters -- duplicates of an
+            // in-range id are still admitted once, by the visited set below
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) {
+              const float sv = __uint_as_float(at[t].x);
+              cand_bits |= (at[t].y < a.n_live && sv >= lo_f && sv <= hi_f) ? 1u << t : 0u;
+            }
+          } else {
             // every first-probe CAS in flight before any is consumed; the table
             // (load <= 1/4) is left all-zero again by undoing this iteration's inserts
             const uint32_t dmask = (1u << dlg) - 1;
