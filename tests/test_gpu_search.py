@@ -142,6 +142,8 @@ def test_wide_ranges_use_exact_hash_visited_set(g):
     for lo, hi in ((-1.0, 2.0), (0.1, 0.8)):
         p = g.SearchParams(k=10, itopk=64, search_width=4, max_iterations=50)
         res = g.search_arrays(gi, Q, lo, hi, p, seed_base=3)
+        fast = g.search_arrays(gi, Q, lo, hi, p, seed_base=3, stats=False)  # no per-iteration unique pass
+        assert np.array_equal(fast.slots, res.slots) and np.array_equal(fast.dists, res.dists)
         for i in range(len(Q)):
             want = beam.beam_search(ox, Q[i], ist.SearchCfg(k=10, lower=lo, upper=hi, itopk=64, search_width=4,
                                                             max_iterations=50, rng_seed=beam.derive_seed(3, i)))
