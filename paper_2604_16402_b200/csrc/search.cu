@@ -215,8 +215,21 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
   const uint32_t lane = lane_id();
   const char* xl = reinterpret_cast<const char*>(X + lane * 4);  // this lane's first column
   const uint32_t rowb = dp * 4;
+  // rolling L2 prefetch, PF rows (~16 KB) ahead of the rows being loaded: deep
+  // enough to cover a round trip, small enough that every warp's prefetched rows
+  // stay L2-resident until used (prefetching a whole iteration of 3.75 KB rows at
+  // d = 960 overran L2 and doubled the DRAM reads)
+  constexpr uint32_t PF = 16384u / (NC * 512u) < (uint32_t)G ? (uint32_t)G : 16384u / (NC * 512u);
+  if (lane < PF && lane < n) {
+    const float* r = X + (uint64_t)cp[lane] * dp;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(r), "r"(rowb) : "memory");
+  }
   __syncwarp();
   for (uint32_t base = 0; base < n; base += G) {
+    if (lane < (uint32_t)G && base + PF + lane < n) {
+      const float* r = X + (uint64_t)cp[base + PF + lane] * dp;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(r), "r"(rowb) : "memory");
+    }
     float4 x[G][NC];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -243,15 +256,6 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
     if ((lane % SPAN) == 0 && base + g < n) cd[base + g] = v;
   }
   __syncwarp();
-}
-
-// Pull every candidate row toward L2 at once (one bulk prefetch per lane per
-// row, no registers held), so score()'s G-row rounds hit L2 instead of HBM.
-__device__ __forceinline__ void prefetch_rows(const float* X, uint32_t dp, const uint32_t* cp, uint32_t n) {
-  for (uint32_t i = lane_id(); i < n; i += 32) {
-    const float* row = X + (uint64_t)cp[i] * dp;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"(dp * 4) : "memory");
-  }
 }
 
 // Pad cp[n .. n+8) with cp[0] so score() can issue whole rounds.
@@ -723,7 +727,6 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           vis_n += nc;
           if (nc == 0) continue;
           dist_evals += nc;
-          prefetch_rows(a.X, a.dp, cp, nc);
           pad_cands(cp, nc);
           score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc);
           L = admit(qe, cd, cs, cp, rr, L, nc, sh.itopk, fu);
