@@ -219,7 +219,11 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
   // enough to cover a round trip, small enough that every warp's prefetched rows
   // stay L2-resident until used (prefetching a whole iteration of 3.75 KB rows at
   // d = 960 overran L2 and doubled the DRAM reads)
-  constexpr uint32_t PF = 16384u / (NC * 512u) < (uint32_t)G ? (uint32_t)G : 16384u / (NC * 512u);
+#ifndef GRAB_PF_BYTES
+#define GRAB_PF_BYTES 16384u
+#endif
+  constexpr uint32_t PF0 = GRAB_PF_BYTES / (NC * 512u);
+  constexpr uint32_t PF = PF0 < (uint32_t)G ? (uint32_t)G : (PF0 > 32u ? 32u : PF0);
   if (lane < PF && lane < n) {
     const float* r = X + (uint64_t)cp[lane] * dp;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(r), "r"(rowb) : "memory");
