@@ -51,6 +51,9 @@ struct DevIndex {
   // neighbour. Rebuilt lazily by the search path when adj_version moved.
   uint64_t adj_version = 1;  // bumped by every adjacency / layout mutation
   mutable Attr* adja = nullptr;
+  // per-stream search scratch (visited tables, overflow list), grown on demand
+  // and reused by later calls on the same stream (search.cu)
+  std::shared_ptr<struct SearchWsCache> search_ws;
   mutable uint64_t adja_rows = 0, adja_version = 0;
   std::shared_ptr<std::mutex> adja_mu = std::make_shared<std::mutex>();
 
@@ -74,6 +77,7 @@ void index_alloc_slots(DevIndex& ix);
 void index_free(DevIndex& ix);
 // (re)build ix.adja if the adjacency changed since the last search (search.cu)
 void ensure_adja(const DevIndex& ix, cudaStream_t st);
+void free_search_ws(DevIndex& ix);
 // Lay out `count` slots whose bucket ids are in ix.i2b (device) and whose
 // vectors/scalars are given in slot order (device pointers, rows of `dim`).
 // Members of a bucket are ordered by ascending slot. Allocates slabs with

@@ -54,6 +54,7 @@ static void free_buckets(DevIndex& ix) {
 }
 
 void index_free(DevIndex& ix) {
+  free_search_ws(ix);
   free_phys(ix);
   free_buckets(ix);
   cfree(ix.slot2phys);

@@ -24,6 +24,9 @@
 // library's one xor tree (bit-identical across kernels).
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <memory>
+#include <mutex>
 
 #include "index.cuh"
 #include "rng.cuh"
@@ -880,13 +883,32 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   epl = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
   if (epl > 4 || sh.cmax > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
   const bool full = a.dp == nc * 128;
-  int per_sm = 1;
-  with_kernel(nc, epl, full, [&](auto kern) {
-    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
-  });
-  per_sm = std::max(per_sm, 1);
+  // launch configuration per (instance, smem): the attribute / occupancy calls
+  // cost tens of microseconds, so they run once per configuration and device
+  int dev = 0;
+  GRAB_CUDA(cudaGetDevice(&dev));
+  const uint64_t key = ((uint64_t)dev << 48) | ((uint64_t)nc << 40) | ((uint64_t)epl << 36) |
+                       ((uint64_t)full << 35) | smem;
+  static std::mutex occ_mu;
+  static std::map<uint64_t, int> occ;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> g(occ_mu);
+    auto it = occ.find(key);
+    if (it != occ.end()) {
+      per_sm = it->second;
+    } else {
+      with_kernel(nc, epl, full, [&](auto kern) {
+        // the attribute is per kernel instance: always the device maximum, so a
+        // later, smaller configuration never lowers it under a cached larger one
+        GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        GRAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
+      });
+      per_sm = std::max(per_sm, 1);
+      occ[key] = per_sm;
+    }
+  }
   const uint64_t blocks =
       std::min<uint64_t>(std::min<uint64_t>(div_up(a.nwork, wpb), (uint64_t)per_sm * num_sms), max_blocks);
   if (!blocks) return;
@@ -904,6 +926,37 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
 // 3/4 load are listed by the main grid and re-run exactly by a second grid with
 // a worst-case table; that grid reads its work count on the device (and exits
 // at once when nothing overflowed).
+// Scratch of one stream: reused by every later search on that stream (stream
+// order makes the reuse safe without host synchronization).
+struct SearchWs {
+  DBufLite tables, big_tables, ovf;
+};
+struct SearchWsCache {
+  std::mutex mu;
+  std::map<cudaStream_t, std::unique_ptr<SearchWs>> by_stream;
+};
+
+void free_search_ws(DevIndex& ix) {
+  if (!ix.search_ws) return;
+  cudaDeviceSynchronize();
+  ix.search_ws->by_stream.clear();  // DBufLite frees stream-ordered
+  cudaDeviceSynchronize();
+  ix.search_ws.reset();
+}
+
+static SearchWs& workspace(const DevIndex& ix, cudaStream_t st) {
+  static std::mutex init_mu;
+  {
+    std::lock_guard<std::mutex> g(init_mu);
+    if (!ix.search_ws) const_cast<DevIndex&>(ix).search_ws = std::make_shared<SearchWsCache>();
+  }
+  SearchWsCache& c = *ix.search_ws;
+  std::lock_guard<std::mutex> g(c.mu);
+  auto& slot = c.by_stream[st];
+  if (!slot) slot = std::make_unique<SearchWs>();
+  return *slot;
+}
+
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
   if (a.width * a.k_max > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
@@ -911,7 +964,10 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   ensure_adja(ix, st);
   a.adja = ix.adja;
   SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp);
-  DBufLite tables, big_tables, ovfb;
+  SearchWs& ws = workspace(ix, st);
+  DBufLite& tables = ws.tables;
+  DBufLite& big_tables = ws.big_tables;
+  DBufLite& ovfb = ws.ovf;
   ovfb.ensure((a.nwork + 1) * sizeof(uint32_t), st);
   uint32_t* ovf = (uint32_t*)ovfb.p;
   GRAB_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
