@@ -393,11 +393,19 @@ def main():
     if args.impl == "reference" and rank != 0:
         return
     import torch
+    # GRAB_BENCH_SHARED_GPU=1 (control-flow testing only): more ranks than GPUs,
+    # ranks share devices and talk over gloo; never set for a measurement
+    shared = os.environ.get("GRAB_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1 and args.impl == "grab":
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2604_16402_b200 as g
     from paper_2604_16402_b200 import datasets as ds
