@@ -366,7 +366,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="grab", choices=["grab", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(PRESETS))
-    ap.add_argument("--n", type=int)
+    ap.add_argument("--rows", "--n", dest="n", type=int, help="rows (per GPU for cfg5)")
     ap.add_argument("--dim", type=int)
     ap.add_argument("--cap", type=int)
     ap.add_argument("--nq", type=int)
