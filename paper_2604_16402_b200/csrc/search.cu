@@ -136,7 +136,7 @@ __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15
 // {f64 distance, slot, phys | kExpanded} kept sorted by (distance, slot), so a
 // merge moves one LDS.128/STS.128 per displaced entry.
 struct WarpLayout {
-  uint32_t qe, cd, cs, cp, rr, dd, fr, q, bytes;
+  uint32_t qe, cd, cs, cp, dd, fr, q, bytes;
 };
 
 __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
@@ -150,8 +150,6 @@ __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
   o += align16(s.cmax * 4);
   l.cp = o;
   o += align16((s.cmax + 8) * 4);
-  l.rr = o;
-  o += 32 * 4;
   l.dd = o;
   o += align16(s.dsz * 4);
   l.fr = o;
@@ -318,10 +316,12 @@ __device__ __forceinline__ uint32_t rank_in_queue(const uint4* qe, uint32_t L, d
 // cannot beat the current tail are dropped first (compacted in place); the
 // survivors are merged 32 at a time (chunk by chunk with truncation after each
 // equals one merge of the union): sorted in registers (network sized to the
-// chunk), ranked against the queue by binary search, and every displaced
-// queue entry moves once. `fu` (first-unexpanded hint) is lowered to the first
-// new entry. Returns the new length.
-__device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, uint32_t* cp, uint32_t* rr, uint32_t L,
+// chunk), each survivor's final position = its index + its rank in the queue
+// (branch-free binary search), and every output position from the first new
+// entry up is filled once, top chunk first, from either a survivor (shuffle)
+// or the queue entry it displaces. `fu` (first-unexpanded hint) is lowered to
+// the first new entry. Returns the new length.
+__device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, uint32_t* cp, uint32_t L,
                                           uint32_t nc, uint32_t itopk, uint32_t& fu) {
   const uint32_t lane = lane_id();
   const double kInf = __longlong_as_double(0x7FF0000000000000ll);
@@ -536,7 +536,6 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
   double* cd = (double*)(base + sh.o_cd);
   uint32_t* cs = (uint32_t*)(base + sh.o_cs);
   uint32_t* cp = (uint32_t*)(base + sh.o_cp);
-  uint32_t* rr = (uint32_t*)(base + sh.o_rr);
   uint32_t* dd = (uint32_t*)(base + sh.o_dd);
   uint32_t* fr = (uint32_t*)(base + sh.o_fr);
   const uint32_t gw = blockIdx.x * wpb + wib;
@@ -582,7 +581,7 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
         pad_cands(cp, ns);
         score<NC, FULL>(qr, a.X, a.dp, cp, cd, ns);
         dist_evals = seed_evals = ns;
-        L = admit(qe, cd, cs, cp, rr, 0, ns, sh.itopk, fu);
+        L = admit(qe, cd, cs, cp, 0, ns, sh.itopk, fu);
         for (uint32_t it = 0; it < a.max_iter; ++it) {
           // frontier: first `width` unexpanded entries (searcher.py:73-79)
           uint32_t nf = 0;
@@ -736,7 +735,7 @@ __global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, 
           dist_evals += nc;
           pad_cands(cp, nc);
           score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc);
-          L = admit(qe, cd, cs, cp, rr, L, nc, sh.itopk, fu);
+          L = admit(qe, cd, cs, cp, L, nc, sh.itopk, fu);
         }
       }
     }
@@ -843,7 +842,6 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   s.o_cd = l.cd;
   s.o_cs = l.cs;
   s.o_cp = l.cp;
-  s.o_rr = l.rr;
   s.o_dd = l.dd;
   s.o_fr = l.fr;
   s.o_q = l.q;

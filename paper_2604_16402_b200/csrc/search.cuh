@@ -45,7 +45,7 @@ struct SearchArgs {
 struct SearchShape {
   uint32_t itopk, width, cmax, dsz, vlog2;
   // per-warp shared-memory layout (byte offsets, filled by make_shape)
-  uint32_t o_qe, o_cd, o_cs, o_cp, o_rr, o_dd, o_fr, o_q, warp_bytes, qbytes;
+  uint32_t o_qe, o_cd, o_cs, o_cp, o_dd, o_fr, o_q, warp_bytes, qbytes;
 };
 
 SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst,
