@@ -251,11 +251,19 @@ __device__ __forceinline__ uint64_t dc_key(float d, uint32_t col) {
 // [C], a compute-flag bitmask [C/32] and an H-entry id hash. First occurrences are found in column order: chunk by
 // chunk, the lowest lane of each id inside the chunk (match_any) inserts it,
 // and an id already present from an earlier chunk is a repeat.
+// jointp = the joint rows with every id mapped to its phys row (-1 kept), so
+// candidate ids index X directly (no dependent slot -> phys load per row)
+__global__ void k_joint_phys(const int32_t* joint, uint64_t total, const uint32_t* s2p, int32_t* jointp) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < total) jointp[i] = joint[i] >= 0 ? (int32_t)s2p[joint[i]] : -1;
+}
+
 template <int WPB>
-__global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint32_t n, uint32_t k,
-                                                      const uint32_t* hop, uint32_t nhop, const uint32_t* s2p,
-                                                      const float* X, uint32_t dp, uint32_t C, uint32_t H,
-                                                      int32_t* out_graph, float* out_dist) {
+__global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, const int32_t* jointp, uint32_t n,
+                                                      uint32_t k, const uint32_t* hop, uint32_t nhop,
+                                                      const uint32_t* s2p, const Attr* attr, const float* X,
+                                                      uint32_t dp, uint32_t C, uint32_t H, int32_t* out_graph,
+                                                      float* out_dist) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
   const uint32_t v = blockIdx.x * WPB + wib;
@@ -266,13 +274,14 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
   uint32_t* fl = (uint32_t*)(base + C * 4);  // bit i of word w: compute column 32 w + i
   uint32_t* hkey = fl + NW;
   const uint32_t J = 2 * k;
-  const int32_t* jv = joint + (uint64_t)v * J;
-  // (a) candidate ids: own joint row, then the joint rows of the hop sources
+  const int32_t* jv = joint + (uint64_t)v * J;  // slot ids (hop sources index the joint rows)
+  const uint32_t pv = s2p[v];
+  // (a) candidate ids in PHYS space: own joint row, then the joint rows of the hop sources
   for (uint32_t i = lane; i < H; i += 32) hkey[i] = 0;
-  for (uint32_t i = lane; i < J; i += 32) cid[i] = jv[i];
+  for (uint32_t i = lane; i < J; i += 32) cid[i] = jointp[(uint64_t)v * J + i];
   for (uint32_t h = 0; h < nhop; ++h) {
     const int32_t src = jv[hop[h]];
-    for (uint32_t i = lane; i < J; i += 32) cid[J + h * J + i] = src >= 0 ? joint[(uint64_t)src * J + i] : -1;
+    for (uint32_t i = lane; i < J; i += 32) cid[J + h * J + i] = src >= 0 ? jointp[(uint64_t)src * J + i] : -1;
   }
   __syncwarp();
   // (b) first occurrence per id, in column order
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
         pend = cur != 0u && cur != (uint32_t)id + 1;
       }
     }
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, lead && cur == 0u && (uint32_t)id != v);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, lead && cur == 0u && (uint32_t)id != pv);
     if (lane == 0) fl[b0 >> 5] = m;
   }
   __syncwarp();
@@ -301,7 +310,6 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
   // (dist, column), 32 columns per chunk: 8-lane group g measures columns
   // c0 + 8g + u (u = 0..7, 4 rows in flight at a time); after the group's
   // xor-reduction lane 8g + s holds column c0 + 8g + s's distance in sums[s].
-  const uint32_t pv = s2p[v];
   const float* qrow = X + (uint64_t)pv * dp;
   const uint32_t sub = lane & 7, grp = lane >> 3;
   uint64_t best = ~0ull;  // lanes >= k never receive real entries
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
       for (int u = 0; u < 4; ++u) {
         const uint32_t bit = grp * 8 + half * 4 + u;
         ok[u] = (flags >> bit) & 1u;
-        pc[u] = ok[u] ? s2p[cid[c0 + bit]] : 0u;
+        pc[u] = ok[u] ? (uint32_t)cid[c0 + bit] : 0u;
       }
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 2
@@ -361,7 +369,8 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, uint
   }
   if (lane < k) {
     const uint32_t col = (uint32_t)best;
-    out_graph[(uint64_t)v * k + lane] = cid[col];
+    const int32_t pid = cid[col];
+    out_graph[(uint64_t)v * k + lane] = pid >= 0 ? (int32_t)attr[pid].slot : -1;
     out_dist[(uint64_t)v * k + lane] = __uint_as_float((uint32_t)(best >> 32));
   }
 }
@@ -468,6 +477,7 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   while (H < C + C / 2) H <<= 1;  // id hash at load <= 2/3 (1088 candidates -> 2048)
   if (H > 65536) throw Error(GRAB_ERR_VALUE, "descent candidate set too large");
   int32_t* joint = S.alloc<int32_t>((uint64_t)n * J);
+  int32_t* jointp = S.alloc<int32_t>((uint64_t)n * J);
   int32_t* g2 = S.alloc<int32_t>(nk);
   float* d2 = S.alloc<float>(nk);
   uint64_t* key2 = S.alloc<uint64_t>(nk);
@@ -505,7 +515,10 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
     GRAB_CHECK_LAUNCH();
     const std::vector<uint32_t> perm = hg.permutation(J);
     GRAB_CUDA(cudaMemcpyAsync(dhop, perm.data(), nhop * 4, cudaMemcpyHostToDevice, st));
-    k_descent<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem, st>>>(joint, n, k, dhop, nhop, ix.slot2phys, ix.X,
+    k_joint_phys<<<(unsigned)div_up((uint64_t)n * J, 256), 256, 0, st>>>(joint, (uint64_t)n * J, ix.slot2phys, jointp);
+    GRAB_CHECK_LAUNCH();
+    k_descent<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem, st>>>(joint, jointp, n, k, dhop, nhop, ix.slot2phys,
+                                                                     ix.attr, ix.X,
                                                                      ix.dp, C, H, g2, d2);
     GRAB_CHECK_LAUNCH();
     std::swap(graph, g2);
