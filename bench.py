@@ -320,8 +320,9 @@ def run_sharded(args, cfg, rank, world, local, dist):
     hi = lo + sel
     Qd = torch.from_numpy(Q).to(dev)
     truth = idx.search(Qd, lo, hi, g.SearchParams(k=10, itopk=16), exact=True)
-    itopk = args.itopk or 384
-    sp = g.SearchParams(k=10, itopk=itopk, search_width=2, max_iterations=200)
+    itopk = args.itopk or 640
+    iters = args.iters or 500
+    sp = g.SearchParams(k=10, itopk=itopk, search_width=2, max_iterations=iters)
     for _ in range(args.warmup):
         res = idx.search(Qd, lo, hi, sp, seed_base=0)
     if dist:
@@ -345,7 +346,7 @@ def run_sharded(args, cfg, rank, world, local, dist):
             "data": "synthetic (low-rank-16 per shard, scalars uniform in the shard's range)",
             "config": {"workload": f"cfg5: {n}x{dim} rows per GPU ({n * world} total), {NQ} range queries at "
                                    f"{int(sel * 100)}% selectivity, k=10, K_max 64 / K_local 32 / k_g 32, itopk {itopk} / "
-                                   f"width 2 / 200 it, NN-descent rounds {args.refine_rounds or 10}",
+                                   f"width 2 / {iters} it, NN-descent rounds {args.refine_rounds or 10}",
                        "rows_per_gpu": n, "queries": NQ, "recall_at_10": round(rec, 4),
                        "routed_queries_rank0": int(res.routed), "index": "bucket-range sharded",
                        "exchange": ("peer-memory stores (CUDA IPC over NVLink)" if args.exchange == "p2p"
@@ -379,6 +380,7 @@ def main():
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="cfg5: fused peer-memory stores (p2p) or NCCL all-to-all of staged blocks")
     ap.add_argument("--itopk", type=int, help="operating point of the cfg4 / cfg5 modes (320 / 512)")
+    ap.add_argument("--iters", type=int, help="max_iterations of the cfg5 operating point (default 500)")
     ap.add_argument("--refine-rounds", type=int, help="NN-descent rounds (reference default 3; cfg5 uses 10)")
     ap.add_argument("--global-pass", default="auto", choices=["auto", "exact", "descent"],
                     help="pass-2 graph: auto = the reference rule (NN-descent above 100K rows)")
