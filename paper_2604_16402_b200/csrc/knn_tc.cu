@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + as);
-      if (row_ok) {
+      {  // every lane runs the chunk loop (the insertion pass below is warp-synchronous)
         const uint32_t cb = job.c0 + t * BN + col0;
         // |b|^2 with +inf for headroom rows / past the tile's end (one broadcast
         // float4 load per 4 columns); the heap key is only built for survivors
@@ -291,16 +291,30 @@ __global__ void __launch_bounds__(kThreads, 1)
               hit |= (uint32_t)(d[j] <= thr) << j;
             }
           }
-          if (hit) {  // rare after the first tiles: columns at or below the K'-th distance
+          // admissible survivors of this chunk (finite, not the row itself, in
+          // range, causal for insert candidates)
+          uint32_t pend = 0;
 #pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) {
-              const uint32_t c = cb + q * 16 + j;
-              if (((hit >> j) & 1u) && d[j] < INFINITY && c != prow && c < job.c1 && !(causal && c > prow)) {
-                const uint64_t key = ((uint64_t)__float_as_uint(d[j]) << 32) | c;
-                if (key < top) {
-                  heap_replace_top(h, KP, key);
-                  top = h[0];
-                }
+          for (uint32_t j = 0; j < 16; ++j) {
+            const uint32_t c = cb + q * 16 + j;
+            pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && d[j] < INFINITY && c != prow && c < job.c1 &&
+                               !(causal && c > prow)) << j;
+          }
+          // heap insertions lane-parallel: every lane takes its NEXT survivor in
+          // the same pass, so a pass costs one sift-down for all lanes at once
+          // (a per-column loop would run one pass per distinct hit column);
+          // per row the keys still arrive in column order
+          while (__any_sync(0xFFFFFFFFu, pend != 0u)) {
+            if (pend) {
+              const uint32_t j = __ffs(pend) - 1;
+              pend &= pend - 1;
+              float dj = d[0];
+#pragma unroll
+              for (uint32_t jj = 1; jj < 16; ++jj) dj = j == jj ? d[jj] : dj;
+              const uint64_t key = ((uint64_t)__float_as_uint(dj) << 32) | (cb + q * 16 + j);
+              if (key < top) {
+                heap_replace_top(h, KP, key);
+                top = h[0];
               }
             }
           }
