@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               hit |= (uint32_t)(d[j] <= thr) << j;
             }
           }
+          if (!__any_sync(0xFFFFFFFFu, hit != 0u)) continue;  // the common case after the first tiles
           // admissible survivors of this chunk (finite, not the row itself, in
           // range, causal for insert candidates)
           uint32_t pend = 0;
