@@ -60,6 +60,7 @@ class ClockSampler:
         self.gpu = gpu
         self.period = period
         self.rows = []  # (sm_mhz, sm_max_mhz, reasons-bitmask)
+        self.durs = []  # ms per sample call (diagnostics)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._nv = None
@@ -68,14 +69,24 @@ class ClockSampler:
             pynvml.nvmlInit()
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            # constant; queried once here -- the call is a driver round trip that
+            # takes 2-60 ms (tools/nvml_probe.py) and stalled launches when sampled
+            self._max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self._nv = None
 
     def _sample(self):
+        t0 = time.perf_counter()
+        try:
+            self._sample_once()
+        finally:
+            self.durs.append((time.perf_counter() - t0) * 1e3)
+
+    def _sample_once(self):
         if self._nv is not None:
             nv = self._nv
             sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
-            mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            mx = self._max_mhz
             rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
             self.rows.append((float(sm), float(mx), int(rs)))
             return
@@ -510,12 +521,22 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
+        host_ms = []
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            th = time.perf_counter()
             res = g.search_arrays(gi, Qd, lod, hid, sp, seed_base=seed_base)
+            host_ms.append((time.perf_counter() - th) * 1e3)
+            if i < args.steps - 1:
+                evs[i].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    marks = [ev0] + evs + [ev1]
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+    print(f"[bench] timed steps ms {[round(x, 2) for x in step_ms]} host-call ms {[round(x, 2) for x in host_ms]} "
+          f"clock samples {len(clk.rows)} sample-call ms max {max(clk.durs, default=0):.1f}", file=sys.stderr, flush=True)
     if dist:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

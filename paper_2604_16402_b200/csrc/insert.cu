@@ -76,6 +76,43 @@ __device__ __forceinline__ double row_dist(const RowRegs<NC>& q, const float* X,
   return warp_sum(acc);
 }
 
+// G candidate rows in flight per round (x: G * NC float4 registers); the
+// distance of row g lands on lanes with lane >> SH == g.
+template <int NC>
+struct Batch {
+  static constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : 2);
+  static constexpr int SH = G == 8 ? 2 : (G == 4 ? 3 : 4);
+};
+
+// Distances from `r` to rows p[0..G) (ok[g] false: row not read, partial 0);
+// same per-lane chain and reduction tree as row_dist, so bit-identical to it.
+template <int NC>
+__device__ __forceinline__ double dist_batch(const RowRegs<NC>& r, const float* X, uint32_t dp,
+                                             const uint32_t (&p)[Batch<NC>::G], const bool (&ok)[Batch<NC>::G]) {
+  constexpr int G = Batch<NC>::G;
+  const uint32_t lane = lane_id();
+  float4 x[G][NC];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t col = (c * 32 + lane) * 4;
+      x[g][c] = (ok[g] && col < dp) ? ldg_nc_f4(X + (uint64_t)p[g] * dp + col) : make_float4(0, 0, 0, 0);
+    }
+  double part[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t col = (c * 32 + lane) * 4;
+      if (col < dp) acc = sq4(x[g][c], r.v[c], acc);
+    }
+    part[g] = acc;
+  }
+  return reduce_scatter<G>(part);
+}
+
 // ------------------------------------------------------------- shared counters
 struct InsertCounters {
   unsigned long long forward_accepted, forward_rejected, reverse_accepted, reverse_rejected;
@@ -198,27 +235,20 @@ __global__ void k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const
     // nearest_kept[j] = min(nearest_kept[j], dist(s, cand j)) for the undecided tail
     RowRegs<NC> r;
     load_row<NC>(r, X, dp, s2p[s]);
-    if constexpr (NC == 1) {
-      // 8 candidate rows in flight per round; reduce_scatter is bit-identical to row_dist
-      const uint32_t col = lane * 4;
-      for (uint32_t j0 = t + 1; j0 < n; j0 += 8) {
-        float4 x[8];
+    {
+      // G candidate rows in flight per round; reduce_scatter is bit-identical to row_dist
+      constexpr int G = Batch<NC>::G, SH = Batch<NC>::SH;
+      for (uint32_t j0 = t + 1; j0 < n; j0 += G) {
+        uint32_t p[G];
+        bool ok[G];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const uint32_t j = j0 + g;
-          x[g] = (j < n && col < dp) ? ldg_nc_f4(X + (uint64_t)s2p[cs[j]] * dp + col) : make_float4(0, 0, 0, 0);
+        for (int g = 0; g < G; ++g) {
+          ok[g] = j0 + g < n;
+          p[g] = ok[g] ? s2p[cs[j0 + g]] : 0u;
         }
-        double part[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) part[g] = sq4(x[g], r.v[0], 0.0);
-        const double dsum = reduce_scatter<8>(part);  // lanes 4g .. 4g+3 hold candidate j0 + g
-        const uint32_t j = j0 + (lane >> 2);
-        if ((lane & 3) == 0 && j < n && dsum < near[j]) near[j] = dsum;
-      }
-    } else {
-      for (uint32_t j = t + 1; j < n; ++j) {
-        double dj = row_dist<NC>(r, X, dp, s2p[cs[j]]);
-        if (lane == 0 && dj < near[j]) near[j] = dj;
+        const double dsum = dist_batch<NC>(r, X, dp, p, ok);
+        const uint32_t j = j0 + (lane >> SH);
+        if ((lane & ((1u << SH) - 1)) == 0 && j < n && dsum < near[j]) near[j] = dsum;
       }
     }
     __syncwarp();
@@ -255,29 +285,28 @@ __global__ void k_req_heads(const unsigned long long* keys, uint64_t n, uint8_t*
   head[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
 }
 
-// Distances from the row in `r` to row entries j0 .. j0+7 of a lane-distributed
-// row (entry j held by lane j % 32 in e[j / 32]); entry j0 + g's distance is
-// returned on lanes 4g .. 4g+3 (SENTINEL / j >= K: +inf). d <= 128 only (NC = 1);
-// bit-identical to row_dist (reduce_scatter pairs like warp_sum).
-__device__ __forceinline__ double dist8(const RowRegs<1>& r, const float* X, uint32_t dp, const uint32_t (&e)[2],
-                                        uint32_t j0, uint32_t K) {
-  const uint32_t lane = lane_id(), col = lane * 4;
-  float4 x[8];
-  bool ok[8];
+// Distances from the row in `r` to row entries j0 .. j0+G-1 of a lane-distributed
+// row (entry j held by lane j % 32 in e[j / 32]), G = Batch<NC>::G rows in
+// flight; entry j0 + g's distance is returned on lanes g << SH .. (g+1) << SH - 1
+// (SENTINEL / j >= K: +inf). Bit-identical to row_dist (reduce_scatter pairs
+// like warp_sum).
+template <int NC>
+__device__ __forceinline__ double dist_entries(const RowRegs<NC>& r, const float* X, uint32_t dp,
+                                               const uint32_t (&e)[2], uint32_t j0, uint32_t K) {
+  constexpr int G = Batch<NC>::G;
+  const uint32_t lane = lane_id();
+  uint32_t p[G];
+  bool ok[G];
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
+  for (int g = 0; g < G; ++g) {
     const uint32_t j = j0 + g;
-    const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
-    ok[g] = j < K && eo != kSentinel;
-    x[g] = (ok[g] && col < dp) ? ldg_nc_f4(X + (uint64_t)eo * dp + col) : make_float4(0, 0, 0, 0);
+    p[g] = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+    ok[g] = j < K && p[g] != kSentinel;
   }
-  double part[8];
-#pragma unroll
-  for (int g = 0; g < 8; ++g) part[g] = sq4(x[g], r.v[0], 0.0);
-  const double sum = reduce_scatter<8>(part);
+  const double sum = dist_batch<NC>(r, X, dp, p, ok);
   bool okl = false;
 #pragma unroll
-  for (int g = 0; g < 8; ++g) okl = (lane >> 2) == (uint32_t)g ? ok[g] : okl;
+  for (int g = 0; g < G; ++g) okl = (lane >> Batch<NC>::SH) == (uint32_t)g ? ok[g] : okl;
   return okl ? sum : __longlong_as_double(0x7FF0000000000000ll);
 }
 
@@ -300,8 +329,6 @@ __global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint
   const uint32_t pv = s2p[v];
   uint32_t* row = adj + (uint64_t)pv * K;
   unsigned long long acc = 0, rej = 0, ev_nec = 0, ev_red = 0;
-  RowRegs<NC> rv;
-  load_row<NC>(rv, X, dp, pv);
   const double kNegInf = -__longlong_as_double(0x7FF0000000000000ll);
   const uint32_t r0 = K > k_local ? k_local : 0;
   uint32_t e[2];
@@ -328,16 +355,10 @@ __global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint
       RowRegs<NC> rq;
       load_row<NC>(rq, X, dp, pq);
       bool ok = true;
-      if constexpr (NC == 1) {
-        for (uint32_t j0 = 0; j0 < K && ok; j0 += 8) {
-          const double dj = dist8(rq, X, dp, e, j0, K);
-          ok = !__any_sync(0xFFFFFFFFu, (lane & 3) == 0 && j0 + (lane >> 2) < K && !(deff < dj));
-        }
-      } else {
-        for (uint32_t j = 0; j < K && ok; ++j) {
-          const uint32_t ej = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
-          ok = deff < row_dist<NC>(rq, X, dp, ej);
-        }
+      constexpr int G = Batch<NC>::G, SH = Batch<NC>::SH;
+      for (uint32_t j0 = 0; j0 < K && ok; j0 += G) {
+        const double dj = dist_entries<NC>(rq, X, dp, e, j0, K);
+        ok = !__any_sync(0xFFFFFFFFu, (lane & ((1u << SH) - 1)) == 0 && j0 + (lane >> SH) < K && !(deff < dj));
       }
       if (!ok) {
         ++rej;
@@ -345,30 +366,19 @@ __global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint
       }
       if (!have_dv) {
         have_dv = true;
-        for (uint32_t j0 = r0; j0 < K; j0 += 8) {
-          if constexpr (NC == 1) {
-            const double dj = dist8(rv, X, dp, e, j0, K);
+        RowRegs<NC> rv;  // v's row is needed only here (q's diversity test is done)
+        load_row<NC>(rv, X, dp, pv);
+        for (uint32_t j0 = r0; j0 < K; j0 += G) {
+          const double dj = dist_entries<NC>(rv, X, dp, e, j0, K);
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              const double dg = __shfl_sync(0xFFFFFFFFu, dj, 4 * g);
-              const uint32_t j = j0 + g;
-              if (j < K && lane == (j & 31)) {
-                if (j & 32)
-                  dv[1] = dg;
-                else
-                  dv[0] = dg;
-              }
-            }
-          } else {
-            for (uint32_t j = j0; j < j0 + 8 && j < K; ++j) {
-              const uint32_t ej = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
-              const double dg = row_dist<NC>(rv, X, dp, ej);
-              if (lane == (j & 31)) {
-                if (j & 32)
-                  dv[1] = dg;
-                else
-                  dv[0] = dg;
-              }
+          for (int g = 0; g < G; ++g) {
+            const double dg = __shfl_sync(0xFFFFFFFFu, dj, g << SH);
+            const uint32_t j = j0 + g;
+            if (j < K && lane == (j & 31)) {
+              if (j & 32)
+                dv[1] = dg;
+              else
+                dv[0] = dg;
             }
           }
         }
@@ -499,49 +509,22 @@ __global__ void k_heal_apply(const unsigned long long* keys, uint64_t nreq, cons
     }
   }
   const uint32_t r0 = K > k_local ? k_local : 0;
-  // distances of the current eviction-region entries [r0, K): 8 rows in flight
-  // per round for d <= 128 (same reduction tree as row_dist), else one by one
+  // distances of the current eviction-region entries [r0, K): G rows in flight
+  // per round (same reduction tree as row_dist); empty entries keep -inf
   d[0] = d[1] = kNegInf;
-  for (uint32_t j0 = r0; j0 < K; j0 += 8) {
-    if constexpr (NC == 1) {
-      float4 x[8];
-      bool okg[8];
+  constexpr int G = Batch<NC>::G, SH = Batch<NC>::SH;
+  for (uint32_t j0 = r0; j0 < K; j0 += G) {
+    const double sum = dist_entries<NC>(vr, X, dp, e, j0, K);
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        const uint32_t j = j0 + g;
-        const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
-        okg[g] = j < K && eo != kSentinel;
-        const uint32_t col = lane * 4;
-        x[g] = (okg[g] && col < dp) ? ldg_nc_f4(X + (uint64_t)eo * dp + col) : make_float4(0, 0, 0, 0);
-      }
-      double part[8];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) part[g] = sq4(x[g], vr.v[0], 0.0);
-      const double sum = reduce_scatter<8>(part);  // lane 4g holds entry j0 + g
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        const double dg = __shfl_sync(0xFFFFFFFFu, sum, 4 * g);
-        const uint32_t j = j0 + g;
-        if (okg[g] && lane == (j & 31)) {
-          if (j & 32)
-            d[1] = dg;
-          else
-            d[0] = dg;
-        }
-      }
-    } else {
-      for (uint32_t g = 0; g < 8; ++g) {
-        const uint32_t j = j0 + g;
-        if (j >= K) break;
-        const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
-        if (eo == kSentinel) continue;  // warp-uniform
-        const double dd = row_dist<NC>(vr, X, dp, eo);
-        if (lane == (j & 31)) {
-          if (j & 32)
-            d[1] = dd;
-          else
-            d[0] = dd;
-        }
+    for (int g = 0; g < G; ++g) {
+      const double dg = __shfl_sync(0xFFFFFFFFu, sum, g << SH);
+      const uint32_t j = j0 + g;
+      const uint32_t eo = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+      if (j < K && eo != kSentinel && lane == (j & 31)) {
+        if (j & 32)
+          d[1] = dg;
+        else
+          d[0] = dg;
       }
     }
   }

@@ -189,3 +189,18 @@ def test_insert_scaled_matches_oracle(g):
     assert [getattr(rep, k) for k in KEYS] == [getattr(t, k) for k in KEYS]
     assert rep.rewired_rows == t.rewired_rows
     assert np.array_equal(gi.adjacency[:11_000], ref.adjacency[:11_000])
+
+
+@pytest.mark.parametrize("d", [150, 300, 700])
+def test_insert_wide_rows_match_oracle(g, d):
+    """d > 128: the multi-chunk (NC = 2, 4, 8) batched distance paths of the
+    forward / rewire / heal kernels give the oracle's rows and counters."""
+    X, S = ist.gen_lowrank(3_600, d, seed=11)
+    cfg = ist.BuildCfg(k_max=8, k_local=4, bucket_capacity=500)
+    ref, _, _ = construct.build(X[:3_000], S[:3_000], cfg, capacity=4_000)
+    gi = g.load_index(ist.container_bytes(ref), g.BuildParams(k_max=8, k_local=4, bucket_capacity=500))
+    rep = g.insert_batch(gi, X[3_000:], S[3_000:])
+    t = ingest.insert(ref, X[3_000:], S[3_000:])
+    assert [getattr(rep, k) for k in KEYS] == [getattr(t, k) for k in KEYS]
+    assert rep.rewired_rows == t.rewired_rows
+    assert np.array_equal(gi.adjacency[:3_600], ref.adjacency[:3_600])
