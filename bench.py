@@ -558,20 +558,29 @@ def main():
         pass
 
     # ---- e2e through the public API with host buffers (H2D + D2H inside the region)
-    Qh = np.ascontiguousarray(Q)
+    # inputs in page-locked host memory (the API then returns page-locked results)
+    Qh = torch.from_numpy(np.ascontiguousarray(Q)).pin_memory()
+    loh = torch.from_numpy(lo).pin_memory()
+    hih = torch.from_numpy(hi).pin_memory()
+    for _ in range(3):  # untimed: allocate the two pinned result sets the loop alternates between
+        rh = g.search_arrays(gi, Qh, loh, hih, sp, seed_base=seed_base)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     e2e_steps = max(3, args.steps // 2)
+    e2e_ms = []
     for _ in range(e2e_steps):
-        rh = g.search_arrays(gi, Qh, lo, hi, sp, seed_base=seed_base)  # with SearchStats, like the timed loop
+        te = time.perf_counter()
+        rh = g.search_arrays(gi, Qh, loh, hih, sp, seed_base=seed_base)  # with SearchStats, like the timed loop
+        e2e_ms.append((time.perf_counter() - te) * 1e3)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t1) / e2e_steps
+    print(f"[bench] e2e steps ms {[round(x, 2) for x in e2e_ms]}", file=sys.stderr, flush=True)
     if dist:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = Q.nbytes + lo.nbytes + hi.nbytes
-    d2h = rh.slots.nbytes + rh.dists.nbytes + rh.counts.nbytes
+    d2h = rh.slots.nbytes + rh.dists.nbytes + rh.counts.nbytes + rh.stats.nbytes
 
     # the CPU baseline searches the same graph: export it before the insert mutates it
     cpu_idx = oracle_index_from(gi) if (rank == 0 and world == 1 and not args.no_cpu) else None

@@ -77,6 +77,19 @@ def _is_dev(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
 
 
+def _is_pinned(a) -> bool:
+    return hasattr(a, "is_pinned") and not _is_dev(a) and bool(a.is_pinned())
+
+
+def _pinned_empty(shape, dtype) -> np.ndarray:
+    """numpy view of a page-locked host buffer (torch's pinned caching allocator)."""
+    import torch
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape))
+    buf = torch.empty(max(n * dt.itemsize, 1), dtype=torch.uint8, pin_memory=True)
+    return buf.numpy()[: n * dt.itemsize].view(dt).reshape(shape)
+
+
 def _live(live_count) -> int:
     return L.LIVE_ALL if live_count is None else int(live_count)
 
@@ -120,10 +133,13 @@ def search_arrays(index: GraphIndex, queries, lower, upper, params: SearchParams
         hi = np.ascontiguousarray(np.atleast_1d(np.asarray(upper, dtype=np.float64)))
         sd = None if seeds is None else np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
         k = params.k
-        slots = np.empty((nq, k), dtype=np.int64)
-        dists = np.empty((nq, k), dtype=np.float64)
-        counts = np.empty(nq, dtype=np.uint32)
-        st = np.empty(nq, dtype=L.STATS_DTYPE) if stats else None
+        # page-locked queries (a pinned torch CPU tensor) get page-locked result
+        # buffers too, so both copies are plain DMA (no pageable staging)
+        alloc = _pinned_empty if _is_pinned(queries) else np.empty
+        slots = alloc((nq, k), np.int64)
+        dists = alloc((nq, k), np.float64)
+        counts = alloc(nq, np.uint32)
+        st = alloc(nq, L.STATS_DTYPE) if stats else None
         mem = L.MEM_HOST
         s_ptr = None
     if d != index.dim:

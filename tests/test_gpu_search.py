@@ -170,3 +170,27 @@ def test_search_argument_errors_and_out_of_span(g, golden):
     assert r.counts.tolist() == [0, 0] and (r.slots == -1).all()  # ranges outside the scalar span
     s, d, c = g.brute_force_arrays(gi, np.stack([q, q]), np.array([5.0, -3.0]), np.array([6.0, -2.0]), 10)
     assert c.tolist() == [0, 0]
+
+
+def test_pinned_and_device_inputs_match_host(g, golden):
+    """Page-locked torch inputs (pinned results) and device tensors give the
+    host-array results bit for bit (the three memory modes of grab_search)."""
+    import torch
+    gold = golden("mid")
+    gi = g.load_index(gold["container"].tobytes())
+    V, _ = ist.gen_synthetic(10_120, 16, "clusters", rng_seed=2)
+    Q = np.ascontiguousarray(V[10_000:10_048])
+    lo, hi = gold["m_sel1_lower"], gold["m_sel1_upper"]
+    p = g.SearchParams(**GRID[0])
+    ref = g.search_arrays(gi, Q, lo, hi, p, seed_base=11)
+    pin = g.search_arrays(gi, torch.from_numpy(Q).pin_memory(), torch.from_numpy(np.asarray(lo)).pin_memory(),
+                          torch.from_numpy(np.asarray(hi)).pin_memory(), p, seed_base=11)
+    dev = g.search_arrays(gi, torch.from_numpy(Q).cuda(), torch.from_numpy(np.asarray(lo)).cuda(),
+                          torch.from_numpy(np.asarray(hi)).cuda(), p, seed_base=11)
+    torch.cuda.synchronize()
+    for r in (pin, dev):
+        sl = r.slots.cpu().numpy() if hasattr(r.slots, "cpu") else r.slots
+        ds = r.dists.cpu().numpy() if hasattr(r.dists, "cpu") else r.dists
+        ct = r.counts.cpu().numpy() if hasattr(r.counts, "cpu") else r.counts
+        assert np.array_equal(ct.astype(np.int64), ref.counts.astype(np.int64))
+        assert np.array_equal(sl, ref.slots) and np.array_equal(ds.view(np.int64), ref.dists.view(np.int64))
