@@ -41,7 +41,7 @@ PRESETS = {
 }
 GRID = [(32, 1, 50), (32, 2, 50), (48, 2, 50), (64, 2, 50), (64, 4, 50), (96, 4, 50), (128, 4, 50), (192, 4, 50),
         (128, 4, 100), (160, 4, 100), (192, 4, 100), (224, 4, 100), (256, 4, 100), (192, 2, 100), (256, 2, 150),
-        (352, 4, 120), (384, 4, 120), (448, 4, 150)] + [(t, 4, 100) for t in range(264, 352, 8)]
+        (352, 4, 120), (384, 4, 120), (416, 4, 150), (448, 4, 150), (512, 4, 150), (512, 4, 200)] + [(t, 4, 100) for t in range(264, 352, 8)]
 
 
 def env_int(k, d):

@@ -190,6 +190,18 @@ static void copy_back(T* host, const DBuf& b, uint64_t n, uint32_t mem, cudaStre
   GRAB_CUDA(cudaMemcpyAsync(host, b.p, n * sizeof(T), cudaMemcpyDeviceToHost, st));
 }
 
+// Device address of a page-locked host buffer (cudaHostAlloc / cudaHostRegister,
+// e.g. torch pin_memory), else nullptr. Null pointers count as mapped.
+static const void* mapped_host(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 static uint64_t live_of(const DevIndex& ix, uint64_t live_count) {
   return live_count == GRAB_LIVE_ALL ? ix.count : std::min<uint64_t>(live_count, ix.count);
 }
@@ -218,6 +230,25 @@ extern "C" int grab_search(const grab_index* h, const float* queries, uint64_t n
         if (!(lower[i * range_stride] <= upper[i * range_stride]))
           throw Error(GRAB_ERR_VALUE, "invalid range: lower > upper");
     }
+    // Zero-copy when every host buffer is page-locked: the kernel reads each
+    // query row / bound over the host link when its warp starts the query and
+    // stores the results straight into host memory, so the copies overlap the
+    // search instead of bracketing it (GRAB_NO_ZERO_COPY=1 disables).
+    bool zc = mem == GRAB_MEM_HOST && ix.dp == ix.dim && !getenv("GRAB_NO_ZERO_COPY");
+    const void* zq = nullptr;
+    const void *zlo = nullptr, *zhi = nullptr, *zsd = nullptr, *zs = nullptr, *zd = nullptr, *zc_ = nullptr,
+               *zst = nullptr;
+    if (zc) {
+      zq = mapped_host(queries);
+      zlo = mapped_host(lower);
+      zhi = mapped_host(upper);
+      zsd = mapped_host(seeds);
+      zs = mapped_host(out_slots);
+      zd = mapped_host(out_dists);
+      zc_ = mapped_host(out_counts);
+      zst = mapped_host(out_stats);
+      zc = zq && ((uintptr_t)zq & 15) == 0 && zlo && zhi && (!seeds || zsd) && zs && zd && zc_ && (!out_stats || zst);
+    }
     DBuf bq, blo, bhi, bseed, bs, bd, bc, bst;
     SearchArgs a{};
     a.X = ix.X;
@@ -231,11 +262,12 @@ extern "C" int grab_search(const grab_index* h, const float* queries, uint64_t n
     a.bcount = ix.bcount;
     a.bcum = ix.bcum;
     a.n_live = live_of(ix, live_count);
-    a.Q = padded_rows(ix, queries, nq, mem, bq, st);
-    a.lower = stage_in(lower, (nr - 1) * range_stride + 1, mem, blo, st);
-    a.upper = stage_in(upper, (nr - 1) * range_stride + 1, mem, bhi, st);
+    const uint32_t smem = zc ? (uint32_t)GRAB_MEM_DEVICE : mem;  // staging mode of the buffers
+    a.Q = zc ? (const float*)zq : padded_rows(ix, queries, nq, mem, bq, st);
+    a.lower = stage_in(zc ? (const double*)zlo : lower, (nr - 1) * range_stride + 1, smem, blo, st);
+    a.upper = stage_in(zc ? (const double*)zhi : upper, (nr - 1) * range_stride + 1, smem, bhi, st);
     a.range_stride = range_stride;
-    a.seeds = stage_in(seeds, nq, mem, bseed, st);
+    a.seeds = stage_in(zc ? (const uint64_t*)zsd : seeds, nq, smem, bseed, st);
     a.seed_base = seed_base;
     a.ordinal0 = ordinal0;
     a.k = p->k;
@@ -244,15 +276,15 @@ extern "C" int grab_search(const grab_index* h, const float* queries, uint64_t n
     a.max_iter = p->max_iterations;
     a.want = p->seed_count ? p->seed_count : std::min<uint32_t>(p->itopk, 32);
     a.nwork = (uint32_t)nq;
-    a.out_slots = stage_out(out_slots, nq * p->k, mem, bs, st);
-    a.out_dists = stage_out(out_dists, nq * p->k, mem, bd, st);
-    a.out_counts = stage_out(out_counts, nq, mem, bc, st);
-    a.out_stats = stage_out(out_stats, nq, mem, bst, st);
+    a.out_slots = stage_out(zc ? (int64_t*)zs : out_slots, nq * p->k, smem, bs, st);
+    a.out_dists = stage_out(zc ? (double*)zd : out_dists, nq * p->k, smem, bd, st);
+    a.out_counts = stage_out(zc ? (uint32_t*)zc_ : out_counts, nq, smem, bc, st);
+    a.out_stats = stage_out(zc ? (grab_search_stats*)zst : out_stats, nq, smem, bst, st);
     run_search(ix, a, st);
-    copy_back(out_slots, bs, nq * p->k, mem, st);
-    copy_back(out_dists, bd, nq * p->k, mem, st);
-    copy_back(out_counts, bc, nq, mem, st);
-    copy_back(out_stats, bst, nq, mem, st);
+    copy_back(out_slots, bs, nq * p->k, smem, st);
+    copy_back(out_dists, bd, nq * p->k, smem, st);
+    copy_back(out_counts, bc, nq, smem, st);
+    copy_back(out_stats, bst, nq, smem, st);
     if (mem == GRAB_MEM_HOST) GRAB_CUDA(cudaStreamSynchronize(st));
   });
 }

@@ -172,9 +172,10 @@ def test_search_argument_errors_and_out_of_span(g, golden):
     assert c.tolist() == [0, 0]
 
 
-def test_pinned_and_device_inputs_match_host(g, golden):
-    """Page-locked torch inputs (pinned results) and device tensors give the
-    host-array results bit for bit (the three memory modes of grab_search)."""
+def test_pinned_and_device_inputs_match_host(g, golden, monkeypatch):
+    """Page-locked torch inputs (pinned results: zero-copy, and staged with
+    GRAB_NO_ZERO_COPY=1) and device tensors give the host-array results bit for
+    bit (the memory modes of grab_search)."""
     import torch
     gold = golden("mid")
     gi = g.load_index(gold["container"].tobytes())
@@ -183,14 +184,20 @@ def test_pinned_and_device_inputs_match_host(g, golden):
     lo, hi = gold["m_sel1_lower"], gold["m_sel1_upper"]
     p = g.SearchParams(**GRID[0])
     ref = g.search_arrays(gi, Q, lo, hi, p, seed_base=11)
-    pin = g.search_arrays(gi, torch.from_numpy(Q).pin_memory(), torch.from_numpy(np.asarray(lo)).pin_memory(),
-                          torch.from_numpy(np.asarray(hi)).pin_memory(), p, seed_base=11)
+    pinned = (torch.from_numpy(Q).pin_memory(), torch.from_numpy(np.asarray(lo)).pin_memory(),
+              torch.from_numpy(np.asarray(hi)).pin_memory())
+    pin = g.search_arrays(gi, *pinned, p, seed_base=11)
+    monkeypatch.setenv("GRAB_NO_ZERO_COPY", "1")
+    staged = g.search_arrays(gi, *pinned, p, seed_base=11)
+    monkeypatch.delenv("GRAB_NO_ZERO_COPY")
     dev = g.search_arrays(gi, torch.from_numpy(Q).cuda(), torch.from_numpy(np.asarray(lo)).cuda(),
                           torch.from_numpy(np.asarray(hi)).cuda(), p, seed_base=11)
     torch.cuda.synchronize()
-    for r in (pin, dev):
+    for r in (pin, staged, dev):
         sl = r.slots.cpu().numpy() if hasattr(r.slots, "cpu") else r.slots
         ds = r.dists.cpu().numpy() if hasattr(r.dists, "cpu") else r.dists
         ct = r.counts.cpu().numpy() if hasattr(r.counts, "cpu") else r.counts
         assert np.array_equal(ct.astype(np.int64), ref.counts.astype(np.int64))
         assert np.array_equal(sl, ref.slots) and np.array_equal(ds.view(np.int64), ref.dists.view(np.int64))
+        if r.stats is not None and not hasattr(r.stats, "cpu"):
+            assert r.stats.tobytes() == ref.stats.tobytes()

@@ -29,7 +29,11 @@ def t(fn, n=10):
 
 
 print("pageable ms", t(lambda: g.search_arrays(gi, Q, lo, hi, sp, seed_base=0)))
-print("pinned   ms", t(lambda: g.search_arrays(gi, Qp, lop, hip, sp, seed_base=0)))
+print("pinned zero-copy ms", t(lambda: g.search_arrays(gi, Qp, lop, hip, sp, seed_base=0)))
+import os
+os.environ["GRAB_NO_ZERO_COPY"] = "1"
+print("pinned staged ms", t(lambda: g.search_arrays(gi, Qp, lop, hip, sp, seed_base=0)))
+del os.environ["GRAB_NO_ZERO_COPY"]
 print("pinned nostats ms", t(lambda: g.search_arrays(gi, Qp, lop, hip, sp, seed_base=0, stats=False)))
 print("alloc4   ms", t(lambda: [api._pinned_empty((nq, 10), np.int64), api._pinned_empty((nq, 10), np.float64),
                                  api._pinned_empty(nq, np.uint32), api._pinned_empty(nq, g._lib.STATS_DTYPE)]))
