@@ -14,7 +14,8 @@ import numpy as np  # noqa: E402
 import paper_2604_16402_b200 as g  # noqa: E402
 from paper_2604_16402_b200 import datasets as ds  # noqa: E402
 
-P = {"cfg1": (100_000, 128, 6250, 1000, 96, 4, 50), "cfg2": (1_000_000, 128, 10_000, 10_000, 256, 4, 100)}
+P = {"cfg1": (100_000, 128, 6250, 1000, 96, 4, 50), "cfg2": (1_000_000, 128, 10_000, 10_000, 256, 4, 100),
+     "cfg3": (1_000_000, 960, 10_000, 10_000, 328, 4, 100)}
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--itopk", type=int)
