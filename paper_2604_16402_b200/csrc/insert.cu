@@ -139,6 +139,8 @@ __global__ void k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const
   uint32_t* cs = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wib * P;  // slot
   uint32_t* acc_s = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wpb * P +
                     (uint64_t)wib * K;  // accepted slots (K)
+  uint16_t* alv = (uint16_t*)((uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) +
+                              (uint64_t)wpb * (P + K)) + (uint64_t)wib * P;  // live tail indices (P)
   const uint64_t q = start + i;
   const uint32_t pq = s2p[q];
   // gather candidates
@@ -232,23 +234,44 @@ __global__ void k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const
       acc_d[nacc] = d;
     }
     ++nacc;
-    // nearest_kept[j] = min(nearest_kept[j], dist(s, cand j)) for the undecided tail
+    // nearest_kept[j] = min(nearest_kept[j], dist(s, cand j)) for the undecided
+    // tail. Only LIVE tail candidates are measured: j with de_j >= nearest_kept[j]
+    // is already rejected whatever happens later (nearest_kept only decreases),
+    // and self is never accepted, so skipping them changes no decision.
     RowRegs<NC> r;
     load_row<NC>(r, X, dp, s2p[s]);
+    uint32_t na = 0;
+    for (uint32_t j0 = t + 1; j0 < n; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      bool live = false;
+      if (j < n) {
+        const uint32_t sj = cs[j];
+        const double dj = cd[j];
+        const double dej = sj >= start ? alpha2 * dj : dj;
+        live = sj != (uint32_t)q && dej < near[j];
+      }
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, live);
+      if (live) alv[na + __popc(m & ((1u << lane) - 1))] = (uint16_t)j;
+      na += __popc(m);
+    }
+    __syncwarp();
     {
       // G candidate rows in flight per round; reduce_scatter is bit-identical to row_dist
       constexpr int G = Batch<NC>::G, SH = Batch<NC>::SH;
-      for (uint32_t j0 = t + 1; j0 < n; j0 += G) {
+      for (uint32_t a0 = 0; a0 < na; a0 += G) {
         uint32_t p[G];
         bool ok[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          ok[g] = j0 + g < n;
-          p[g] = ok[g] ? s2p[cs[j0 + g]] : 0u;
+          ok[g] = a0 + g < na;
+          p[g] = ok[g] ? s2p[cs[alv[a0 + g]]] : 0u;
         }
         const double dsum = dist_batch<NC>(r, X, dp, p, ok);
-        const uint32_t j = j0 + (lane >> SH);
-        if ((lane & ((1u << SH) - 1)) == 0 && j < n && dsum < near[j]) near[j] = dsum;
+        const uint32_t a = a0 + (lane >> SH);
+        if ((lane & ((1u << SH) - 1)) == 0 && a < na) {
+          const uint32_t j = alv[a];
+          if (dsum < near[j]) near[j] = dsum;
+        }
       }
     }
     __syncwarp();
@@ -809,7 +832,7 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
   while (P < KL + (n0 > 0 ? KS : 0)) P <<= 1;
   {
     const uint32_t wpb = 4;
-    size_t smem = (size_t)wpb * (P * (8 + 8 + 4) + K * (8 + 4));
+    size_t smem = (size_t)wpb * (P * (8 + 8 + 4 + 2) + K * (8 + 4));
     by_nc(ix.dp, [&](auto ncv) {
       constexpr int NC = decltype(ncv)::value;
       auto kern = k_forward<NC>;
