@@ -55,7 +55,16 @@ struct DevIndex {
   // and reused by later calls on the same stream (search.cu)
   std::shared_ptr<struct SearchWsCache> search_ws;
   mutable uint64_t adja_rows = 0, adja_version = 0;
-  std::shared_ptr<std::mutex> adja_mu = std::make_shared<std::mutex>();
+  // guards adja; `ready` is recorded after a rebuild so searches on other
+  // streams wait for it instead of reading a half-filled mirror
+  struct AdjaSync {
+    std::mutex mu;
+    cudaEvent_t ready = nullptr;
+    ~AdjaSync() {
+      if (ready) cudaEventDestroy(ready);
+    }
+  };
+  std::shared_ptr<AdjaSync> adja_sync = std::make_shared<AdjaSync>();
 
   // buckets
   uint32_t m = 0;

@@ -793,8 +793,12 @@ __global__ void k_fill_adja(const uint32_t* __restrict__ adj, const Attr* __rest
 }
 
 void ensure_adja(const DevIndex& ix, cudaStream_t st) {
-  std::lock_guard<std::mutex> lk(*ix.adja_mu);
-  if (ix.adja && ix.adja_rows == ix.phys_cap && ix.adja_version == ix.adj_version) return;
+  DevIndex::AdjaSync& sy = *ix.adja_sync;
+  std::lock_guard<std::mutex> lk(sy.mu);
+  if (ix.adja && ix.adja_rows == ix.phys_cap && ix.adja_version == ix.adj_version) {
+    if (sy.ready) GRAB_CUDA(cudaStreamWaitEvent(st, sy.ready, 0));  // (free once the fill has run)
+    return;
+  }
   const uint64_t n = ix.phys_cap * ix.params.k_max;
   if (!ix.adja || ix.adja_rows != ix.phys_cap) {
     if (ix.adja) {
@@ -810,6 +814,8 @@ void ensure_adja(const DevIndex& ix, cudaStream_t st) {
     GRAB_CHECK_LAUNCH();
   }
   ix.adja_version = ix.adj_version;
+  if (!sy.ready) GRAB_CUDA(cudaEventCreateWithFlags(&sy.ready, cudaEventDisableTiming));
+  GRAB_CUDA(cudaEventRecord(sy.ready, st));
 }
 
 // ---------------------------------------------------------------- host
@@ -927,6 +933,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
 // Scratch of one stream: reused by every later search on that stream (stream
 // order makes the reuse safe without host synchronization).
 struct SearchWs {
+  std::mutex mu;  // host-side: one enqueue at a time per stream (threads may share a stream)
   DBufLite tables, big_tables, ovf;
 };
 struct SearchWsCache {
@@ -963,6 +970,7 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.adja = ix.adja;
   SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp);
   SearchWs& ws = workspace(ix, st);
+  std::lock_guard<std::mutex> ws_lock(ws.mu);
   DBufLite& tables = ws.tables;
   DBufLite& big_tables = ws.big_tables;
   DBufLite& ovfb = ws.ovf;

@@ -201,3 +201,57 @@ def test_pinned_and_device_inputs_match_host(g, golden, monkeypatch):
         assert np.array_equal(sl, ref.slots) and np.array_equal(ds.view(np.int64), ref.dists.view(np.int64))
         if r.stats is not None and not hasattr(r.stats, "cpu"):
             assert r.stats.tobytes() == ref.stats.tobytes()
+
+
+def test_concurrent_searches_match_sequential(g, golden):
+    """Readers are concurrent-safe (SPEC: per-thread visited table): threads
+    sharing the index -- host calls on the index stream, device calls on their
+    own streams, with shapes that regrow the per-stream scratch -- return the
+    sequential results."""
+    import threading
+
+    import torch
+    gold = golden("mid")
+    gi = g.load_index(gold["container"].tobytes())
+    V, _ = ist.gen_synthetic(10_120, 16, "clusters", rng_seed=2)
+    Q = np.ascontiguousarray(V[10_000:10_120])
+    lo = np.concatenate([gold["m_sel2_lower"], gold["m_sel1_lower"], gold["m_sel3_lower"]])
+    hi = np.concatenate([gold["m_sel2_upper"], gold["m_sel1_upper"], gold["m_sel3_upper"]])
+    Qs = [Q[:48], Q[48:96], Q[72:120]]
+    los = [lo[:48], lo[48:96], lo[72:120]]
+    his = [hi[:48], hi[48:96], hi[72:120]]
+    plist = [g.SearchParams(k=10, itopk=t, search_width=4, max_iterations=60) for t in (32, 128, 256, 512)]
+    want = {(qi, pi): g.search_arrays(gi, Qs[qi], los[qi], his[qi], p, seed_base=7)
+            for qi in range(3) for pi, p in enumerate(plist)}
+    got, errs = {}, []
+
+    def worker(tid):
+        try:
+            dev = tid % 2 == 1
+            st = torch.cuda.Stream() if dev else None
+            for rep in range(3):
+                for qi in range(3):
+                    for pi in ([0, 1, 2, 3] if (tid + rep) % 2 else [3, 2, 1, 0]):
+                        if dev:
+                            with torch.cuda.stream(st):
+                                r = g.search_arrays(gi, torch.from_numpy(Qs[qi]).cuda(),
+                                                    torch.from_numpy(np.asarray(los[qi])).cuda(),
+                                                    torch.from_numpy(np.asarray(his[qi])).cuda(), plist[pi],
+                                                    seed_base=7)
+                                st.synchronize()
+                            got[(tid, rep, qi, pi)] = r.slots.cpu().numpy()
+                        else:
+                            got[(tid, rep, qi, pi)] = g.search_arrays(gi, Qs[qi], los[qi], his[qi], plist[pi],
+                                                                      seed_base=7).slots
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert len(got) == 4 * 3 * 3 * 4
+    for (tid, rep, qi, pi), sl in got.items():
+        assert np.array_equal(sl, want[(qi, pi)].slots), (tid, rep, qi, pi)
