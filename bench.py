@@ -459,11 +459,14 @@ def main():
         sp = g.SearchParams(k=10, itopk=itopk, search_width=width, max_iterations=iters)
         r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=seed_base)
         rec = ds.batch_recall(r.slots, r.counts, truth, tcnt, 10)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        g.search_arrays(gi, Qd, lod, hid, sp, seed_base=seed_base, stats=False)
-        torch.cuda.synchronize()
-        q = nq / (time.perf_counter() - t1)
+        ts = []
+        for _ in range(3):  # median of 3: one noisy timing must not pick the operating point
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            g.search_arrays(gi, Qd, lod, hid, sp, seed_base=seed_base, stats=False)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t1)
+        q = nq / sorted(ts)[1]
         if dist:  # every rank must pick the same operating point: global recall, slowest rank's QPS
             t = torch.tensor([rec, -q], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
