@@ -210,10 +210,20 @@ def _timed(fn, stream):
     return e0.elapsed_time(e1), out
 
 
+def _warm_build(g, ds, dim, params, device, global_pass):
+    """One untimed 120K-row build with the same kernels (pass 1, NN-descent above
+    100K rows, fuse): loads the lazily-loaded CUDA modules and grows the
+    stream-ordered memory pool, so build_s is the steady-state build time."""
+    Xw, Sw = ds.gen_lowrank(120_000, dim, seed=7)
+    gw, _ = g.build_index(Xw, Sw, params, device=device, global_pass=global_pass)
+    del gw
+
+
 def _gpu_warm(device: int, seconds: float = 0.5):
     """Keep the GPU busy (bf16 matmuls) for `seconds` so clocks are up before a
     one-shot measurement."""
     import torch
+    seconds = float(os.environ.get("GRAB_BENCH_GPU_WARM_S", seconds))
     a = torch.randn(4096, 4096, device=f"cuda:{device}", dtype=torch.bfloat16)
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < seconds:
@@ -247,6 +257,7 @@ def run_dynamic(args, cfg, rank, world, local, dist):
     total, batch = args.inserts or cfg["inserts"], cfg["batch"]
     X, S = ds.gen_lowrank(n + total, dim, seed=0)
     params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
+    _warm_build(g, ds, dim, params, local, args.global_pass)
     _gpu_warm(local)
     t0 = time.perf_counter()
     gi, brep = g.build_index(X[:n], S[:n], params, capacity=n + total, device=local, global_pass=args.global_pass)
@@ -439,6 +450,7 @@ def main():
     # ---- build (replicated per rank; deterministic). A fresh process starts on an
     # idle GPU whose clocks ramp over the first ~0.5 s of work; spin the GPU for a
     # moment first so build_s measures the build, not the clock ramp.
+    _warm_build(g, ds, dim, params, local, args.global_pass)
     _gpu_warm(local)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -490,7 +502,9 @@ def main():
               "k": 10, "itopk": itopk, "search_width": width, "max_iterations": iters, "recall_at_10": recall,
               "k_max": 32, "k_local": 16, "l2": f"inputs larger than L2 (X = {n * dim * 4 / 1e6:.0f} MB > 126 MB)",
               "index": "replicated per GPU" if world > 1 else "single GPU",
-              "global_pass": brep.global_pass}
+              "global_pass": brep.global_pass,
+              "build_timing": "host wall clock of build_index (host arrays in, upload included) after one "
+                              "untimed 120K-row warm-up build (CUDA module load, memory pool)"}
 
     if args.impl == "reference":
         procs = os.cpu_count() or 1
@@ -521,25 +535,44 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
-        host_ms = []
-        ev0.record(stream)
-        for i in range(args.steps):
-            th = time.perf_counter()
-            res = g.search_arrays(gi, Qd, lod, hid, sp, seed_base=seed_base)
-            host_ms.append((time.perf_counter() - th) * 1e3)
-            if i < args.steps - 1:
-                evs[i].record(stream)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    marks = [ev0] + evs + [ev1]
-    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
-    print(f"[bench] timed steps ms {[round(x, 2) for x in step_ms]} host-call ms {[round(x, 2) for x in host_ms]} "
-          f"clock samples {len(clk.rows)} sample-call ms max {max(clk.durs, default=0):.1f}", file=sys.stderr, flush=True)
+    def timed_region():
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
+            host_ms = []
+            ev0.record(stream)
+            for i in range(args.steps):
+                th = time.perf_counter()
+                res = g.search_arrays(gi, Qd, lod, hid, sp, seed_base=seed_base)
+                host_ms.append((time.perf_counter() - th) * 1e3)
+                if i < args.steps - 1:
+                    evs[i].record(stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        marks = [ev0] + evs + [ev1]
+        step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+        print(f"[bench] timed steps ms {[round(x, 2) for x in step_ms]} host-call ms "
+              f"{[round(x, 2) for x in host_ms]} clock samples {len(clk.rows)} sample-call ms max "
+              f"{max(clk.durs, default=0):.1f}", file=sys.stderr, flush=True)
+        return ev0.elapsed_time(ev1), res, clk
+
+    ms, res, clk = timed_region()
+    # The operating-point probe timed this exact search (without SearchStats) a
+    # moment ago. A timed loop far slower than it means the box was perturbed
+    # (seen a few times: every step ~2-4x slower, clocks normal): re-measure once
+    # and say so in the line, like a throttled run.
+    probe_ms = nq / point[3] * 1e3
+    slow = torch.tensor([1.0 if ms / args.steps > 1.4 * probe_ms else 0.0], device=dev)
+    if dist:
+        dist.all_reduce(slow, op=dist.ReduceOp.MAX)
+    remeasured = None
+    if float(slow.item()) > 0:
+        remeasured = {"first_ms_per_step": round(ms / args.steps, 4), "probe_ms": round(probe_ms, 4),
+                      "why": "timed loop > 1.4x the operating-point probe of the same search"}
+        if dist:
+            dist.barrier()
+        ms, res, clk = timed_region()
     if dist:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -617,6 +650,8 @@ def main():
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/search_traffic.json)"},
             # per step: the search grid + the (normally empty) overflow-retry grid
             "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "sweep": sweep}
+    if remeasured:
+        line["remeasured"] = remeasured
     if cpu_idx is not None:
         procs = os.cpu_count() or 1
         idx = cpu_idx

@@ -348,11 +348,13 @@ def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None =
                                 refine_rounds, mem, C.byref(rep), C.byref(dbg) if dbg is not None else None))
     index._ids[:n] = np.arange(n)
     index._touch()
-    meta = index.meta
-    report = BuildReport(n=int(rep.n), m=int(rep.m), phase1_seconds=rep.phase1_seconds,
+    m = int(rep.m)
+    # bucket sizes from the M_B2I offsets alone (the full meta view is built lazily)
+    off = index._read(L.ARR_B2I_OFFSETS, 0, m + 1, "<u8", (m + 1,)) if m else np.zeros(1, "<u8")
+    report = BuildReport(n=int(rep.n), m=m, phase1_seconds=rep.phase1_seconds,
                          phase2_seconds=rep.phase2_seconds, fuse_seconds=rep.fuse_seconds,
                          total_seconds=rep.total_seconds,
-                         bucket_sizes=[len(b) for b in meta.bucket_to_index] if meta else [],
+                         bucket_sizes=np.diff(off.astype(np.int64)).tolist(),
                          isolated_nodes=int(rep.isolated_nodes),
                          cross_bucket_edge_ratio=float(rep.cross_bucket_edge_ratio),
                          global_pass="descent" if rep.global_descent else "exact")

@@ -269,15 +269,17 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, cons
   const uint32_t v = blockIdx.x * WPB + wib;
   if (v >= n) return;  // warp-uniform
   const uint32_t NW = (C + 31) / 32;  // flag words
-  uint8_t* base = smem + (size_t)wib * (C * 4 + NW * 4 + H * 4);
+  uint8_t* base = smem + (size_t)wib * (C * 4 + NW * 4 + H * 2);
   int32_t* cid = (int32_t*)base;
   uint32_t* fl = (uint32_t*)(base + C * 4);  // bit i of word w: compute column 32 w + i
-  uint32_t* hkey = fl + NW;
+  // id hash of 16-bit entries = first column + 1 (the id itself is cid[entry - 1]):
+  // half the shared memory of an id table, so more warps stay resident
+  unsigned short* hkey = (unsigned short*)(fl + NW);
   const uint32_t J = 2 * k;
   const int32_t* jv = joint + (uint64_t)v * J;  // slot ids (hop sources index the joint rows)
   const uint32_t pv = s2p[v];
   // (a) candidate ids in PHYS space: own joint row, then the joint rows of the hop sources
-  for (uint32_t i = lane; i < H; i += 32) hkey[i] = 0;
+  for (uint32_t i = lane; i < H / 2; i += 32) reinterpret_cast<uint32_t*>(hkey)[i] = 0u;
   for (uint32_t i = lane; i < J; i += 32) cid[i] = jointp[(uint64_t)v * J + i];
   for (uint32_t h = 0; h < nhop; ++h) {
     const int32_t src = jv[hop[h]];
@@ -293,13 +295,14 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, cons
     const uint32_t same = __match_any_sync(0xFFFFFFFFu, (uint32_t)id);
     const bool lead = id >= 0 && (uint32_t)(__ffs(same) - 1) == lane;
     uint32_t h = ((uint32_t)id * 0x9E3779B1u) & hmask;
-    uint32_t cur = lead ? atomicCAS(hkey + h, 0u, (uint32_t)id + 1) : 0u;
-    bool pend = lead && cur != 0u && cur != (uint32_t)id + 1;
+    const unsigned short me = (unsigned short)(c + 1);
+    uint32_t cur = lead ? atomicCAS(hkey + h, (unsigned short)0, me) : 0u;
+    bool pend = lead && cur != 0u && cid[cur - 1] != id;
     while (__any_sync(0xFFFFFFFFu, pend)) {
       if (pend) {
         h = (h + 1) & hmask;
-        cur = atomicCAS(hkey + h, 0u, (uint32_t)id + 1);
-        pend = cur != 0u && cur != (uint32_t)id + 1;
+        cur = atomicCAS(hkey + h, (unsigned short)0, me);
+        pend = cur != 0u && cid[cur - 1] != id;
       }
     }
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, lead && cur == 0u && (uint32_t)id != pv);
@@ -475,7 +478,7 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   const uint32_t C = J + nhop * J;
   uint32_t H = 1;
   while (H < C + C / 2) H <<= 1;  // id hash at load <= 2/3 (1088 candidates -> 2048)
-  if (H > 65536) throw Error(GRAB_ERR_VALUE, "descent candidate set too large");
+  if (C >= 65535 || H > 65536) throw Error(GRAB_ERR_VALUE, "descent candidate set too large");
   int32_t* joint = S.alloc<int32_t>((uint64_t)n * J);
   int32_t* jointp = S.alloc<int32_t>((uint64_t)n * J);
   int32_t* g2 = S.alloc<int32_t>(nk);
@@ -492,7 +495,7 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   int end_bit = 1;
   while ((1ull << end_bit) <= n) ++end_bit;
   constexpr int WPB = 1;
-  const size_t smem = (size_t)WPB * (C * 4 + (C + 31) / 32 * 4 + H * 4);
+  const size_t smem = (size_t)WPB * (C * 4 + (C + 31) / 32 * 4 + H * 2);
   GRAB_CUDA(cudaFuncSetAttribute(k_descent<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (uint32_t r = 0; r < rounds; ++r) {
     // reverse top-k: stable sort by (dist, src), then by dst
