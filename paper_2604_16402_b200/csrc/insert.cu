@@ -123,8 +123,14 @@ struct InsertCounters {
 // Warp per fresh node (slot start + i): union of in-bucket candidates (phys,
 // f64) and search results (slot, f64) -> sort by (dist, slot) -> dedup ->
 // nearest pre-batch -> greedy Eq.1/Eq.2 selection -> forward row + requests.
+#ifndef GRAB_INSERT_MINB
+#define GRAB_INSERT_MINB 6
+#endif
+// (128 threads, >= GRAB_INSERT_MINB blocks/SM: <= 80 registers for NC <= 2, so
+// 24 warps per SM hide the row-load latency: forward 16.9 -> 14.6 ms at cfg2;
+// wide rows keep their registers. k_rewire spills at 80-96 and stays at 128.)
 template <int NC>
-__global__ void k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const Attr* attr, const int32_t* i2b,
+__global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward(uint64_t start, uint64_t b, const uint32_t* s2p, const Attr* attr, const int32_t* i2b,
                           const float* X, uint32_t dp, uint32_t* adj, uint32_t K, const uint32_t* loc_ids,
                           const double* loc_d, uint32_t KL, const int64_t* found_slots, const double* found_d,
                           const uint32_t* found_cnt, uint32_t KS, double alpha2, uint32_t P,
