@@ -633,12 +633,35 @@ def main():
     Xi, Si = ds.gen_lowrank(ins_b, dim, seed=2, w_seed=0)  # in-distribution new rows (same basis)
     Xi_d = torch.from_numpy(Xi).to(dev)
     Si_d = torch.from_numpy(Si).to(dev)
+    # the insert's candidate search (itopk = k = 128, width 4, 50 it, full range)
+    # re-run untimed with SearchStats on the pre-insert index, for the bytes model
+    n0 = gi.count
+    isp = g.SearchParams(k=128, itopk=128, search_width=4, max_iterations=50)
+    ist_ = g.search_arrays(gi, Xi_d, 0.0, 1.0, isp, seed_base=0).stats
+    from paper_2604_16402_b200 import _lib as _glib
+    ins_search_stats = np.frombuffer(ist_.cpu().numpy().astype(np.uint32).tobytes(), dtype=_glib.STATS_DTYPE)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     irep = g.insert_batch(gi, Xi_d, Si_d)
     torch.cuda.synchronize()
     ins_s = time.perf_counter() - t2
     insert_vps = ins_b / ins_s
+    dpi = (dim + 3) // 4 * 4
+    ins_bytes = {  # algorithmic bytes of the batch (SURVEY §8(d) insert work model)
+        "candidate_search": algorithmic_bytes(ins_search_stats, dpi, 32, 128),
+        "bucket_candidates": (n0 + ins_b) * 4.0 * dpi,
+        "forward_select": (irep.forward_accepted + irep.forward_rejected) * 4.0 * dpi,
+        "reverse_rewire": (irep.reverse_accepted + irep.reverse_rejected) * 4.0 * 32
+                          + (irep.evictions_necessary + irep.evictions_redundant) * 32 * 4.0 * dpi,
+        "writes": ins_b * (4.0 * dpi + 4.0 * 32),
+    }
+    ins_total = sum(ins_bytes.values())
+    insert_roofline = {"bound": "hbm", "achieved": round(ins_total / ins_s / 1e9, 1), "peak": hbm,
+                       "unit": "GB/s", "model_bytes_per_vector": round(ins_total / ins_b, 1),
+                       "model_bytes_by_phase": {k: round(v) for k, v in ins_bytes.items()},
+                       "model": "candidate search from an identical stats-on search; every candidate / "
+                                "bucket member / contested row read once"}
+    insert_roofline["frac"] = round(insert_roofline["achieved"] / insert_roofline["peak"], 4)
 
     line = {"metric": "range-filtered QPS @ recall@10=0.95", "value": round(qps, 1), "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -647,7 +670,7 @@ def main():
             "build_s": round(build_s, 3), "build_times_s": [round(x, 3) for x in build_times],
             "build_report": brep.to_dict() | {"bucket_sizes": None},
             "insert_vectors_per_s": round(insert_vps, 1),
-            "insert": {"batch": ins_b, "seconds": round(ins_s, 4), "into": n,
+            "insert": {"batch": ins_b, "seconds": round(ins_s, 4), "into": n, "roofline": insert_roofline,
                        "report": {k: v for k, v in irep.to_dict().items() if k != "rewired_rows"}},
             "e2e": {"value": round(world * nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
