@@ -15,6 +15,8 @@ namespace grab {
 
 constexpr uint32_t BM = kKnnBM, BN = 128, BK = 32;
 constexpr uint32_t kMargin = 16;
+constexpr uint32_t kScreenTileBytes =
+    (BK * (BM + 4) + BK * (BN + 4)) * 4 > BM * (BN + 1) * 4 ? (BK * (BM + 4) + BK * (BN + 4)) * 4 : BM * (BN + 1) * 4;
 
 // Max-heap (h[0] largest) of one row, element i at h[i * BM]: rows are
 // interleaved so neighbouring threads hit neighbouring banks.
@@ -44,8 +46,11 @@ __global__ void __launch_bounds__(256) k_knn_screen(const KnnJob* jobs, const fl
   extern __shared__ __align__(16) uint8_t smem[];
   float* As = (float*)smem;                 // [BK][BM + 4]
   float* Bs = As + BK * (BM + 4);           // [BK][BN + 4]
-  float* D = Bs + BK * (BN + 4);            // [BM][BN + 1]
-  uint64_t* H = (uint64_t*)(D + BM * (BN + 1));  // [BM][KP]
+  // the distance tile is written only after a column block's k-loop and read
+  // before the next one starts (both fenced by __syncthreads), so it shares the
+  // operand tiles' words -- room for K' up to ~150 heaps (insert at K_max 64)
+  float* D = (float*)smem;                  // [BM][BN + 1]
+  uint64_t* H = (uint64_t*)(smem + kScreenTileBytes);  // [BM][KP]
   const KnnJob job = jobs[blockIdx.x];
   const uint32_t t = threadIdx.x;
   const uint32_t ty = t >> 4, tx = t & 15;  // 16 x 16 threads, 8 x 8 outputs each
@@ -226,8 +231,7 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
   if (use_tc) {
     knn_screen_tc(ix, norms, dj, (uint32_t)jobs.size(), KP, cand, causal, st);
   } else {
-    size_t smem = (size_t)BK * (BM + 4) * 4 + (size_t)BK * (BN + 4) * 4 + (size_t)BM * (BN + 1) * 4 +
-                  (size_t)BM * KP * 8;
+    size_t smem = (size_t)kScreenTileBytes + (size_t)BM * KP * 8;
     if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "k too large for the kNN screen");
     GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_knn_screen<<<(unsigned)jobs.size(), 256, smem, st>>>(dj, ix.X, ix.attr, norms, ix.dp, KP, cand, causal);

@@ -525,7 +525,7 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
 #define GRAB_SEARCH_MINB 6
 #endif
 template <int NC, int EPL, bool FULL>
-__global__ void __launch_bounds__(128, GRAB_SEARCH_MINB) k_search(SearchArgs a, SearchShape sh) {
+__global__ void __launch_bounds__(128, EPL >= 8 ? 4 : GRAB_SEARCH_MINB) k_search(SearchArgs a, SearchShape sh) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t lt = (1u << lane) - 1;
@@ -868,6 +868,7 @@ static void with_kernel(uint32_t nc, uint32_t epl, bool full, F&& f) {
   }
   GRAB_K(1, 1) GRAB_K(1, 2) GRAB_K(1, 4) GRAB_K(2, 1) GRAB_K(2, 2) GRAB_K(2, 4)
   GRAB_K(4, 1) GRAB_K(4, 2) GRAB_K(4, 4) GRAB_K(8, 1) GRAB_K(8, 2) GRAB_K(8, 4)
+  GRAB_K(1, 8) GRAB_K(2, 8) GRAB_K(4, 8) GRAB_K(8, 8)  // width * K_max up to 256 (e.g. K_max 64, width 4)
 #undef GRAB_K
   throw Error(GRAB_ERR_VALUE, "unsupported search kernel shape");
 }
@@ -885,7 +886,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   if (!nc) throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported by the search kernel");
   uint32_t epl = (uint32_t)div_up(sh.width * a.k_max, 32);
   epl = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
-  if (epl > 4 || sh.cmax > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
+  if (epl > 8 || sh.cmax > 256) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 256 not supported");
   const bool full = a.dp == nc * 128;
   // launch configuration per (instance, smem): the attribute / occupancy calls
   // cost tens of microseconds, so they run once per configuration and device
@@ -964,7 +965,7 @@ static SearchWs& workspace(const DevIndex& ix, cudaStream_t st) {
 
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
-  if (a.width * a.k_max > 128) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 128 not supported");
+  if (a.width * a.k_max > 256) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 256 not supported");
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);
   a.adja = ix.adja;

@@ -204,3 +204,17 @@ def test_insert_wide_rows_match_oracle(g, d):
     assert [getattr(rep, k) for k in KEYS] == [getattr(t, k) for k in KEYS]
     assert rep.rewired_rows == t.rewired_rows
     assert np.array_equal(gi.adjacency[:3_600], ref.adjacency[:3_600])
+
+
+def test_insert_kmax64_matches_oracle(g):
+    """K_max = 64 (the paper's scale setting): the insert's candidate search runs
+    at width 4 x 64 = 256 neighbours per iteration; rows and counters equal the oracle."""
+    X, S = ist.gen_lowrank(4_400, 16, seed=12)
+    cfg = ist.BuildCfg(k_max=64, k_local=32, bucket_capacity=1000)
+    ref, _, _ = construct.build(X[:4_000], S[:4_000], cfg, capacity=5_000)
+    gi = g.load_index(ist.container_bytes(ref), g.BuildParams(k_max=64, k_local=32, bucket_capacity=1000))
+    rep = g.insert_batch(gi, X[4_000:], S[4_000:])
+    t = ingest.insert(ref, X[4_000:], S[4_000:])
+    assert [getattr(rep, k) for k in KEYS] == [getattr(t, k) for k in KEYS]
+    assert rep.rewired_rows == t.rewired_rows
+    assert np.array_equal(gi.adjacency[:4_400], ref.adjacency[:4_400])

@@ -162,7 +162,7 @@ def test_search_argument_errors_and_out_of_span(g, golden):
     with pytest.raises(ValueError):
         g.search_arrays(gi, q, 0.5, 0.4, g.SearchParams(k=10, itopk=64))  # lower > upper
     with pytest.raises(ValueError):
-        g.search_arrays(gi, q, 0.0, 1.0, g.SearchParams(k=10, itopk=64, search_width=16))  # width*K > 128
+        g.search_arrays(gi, q, 0.0, 1.0, g.SearchParams(k=10, itopk=64, search_width=32))  # width*K > 256
     with pytest.raises(g.DimensionMismatchError):
         g.search_arrays(gi, np.zeros(9, np.float32), 0.0, 1.0, g.SearchParams(k=10, itopk=64))
     r = g.search_arrays(gi, np.stack([q, q]), np.array([5.0, -3.0]), np.array([6.0, -2.0]),
@@ -255,3 +255,23 @@ def test_concurrent_searches_match_sequential(g, golden):
     assert len(got) == 4 * 3 * 3 * 4
     for (tid, rep, qi, pi), sl in got.items():
         assert np.array_equal(sl, want[(qi, pi)].slots), (tid, rep, qi, pi)
+
+
+@pytest.mark.parametrize("kmax,width", [(64, 4), (32, 8), (16, 16)])
+def test_wide_fanout_search_matches_oracle(g, kmax, width):
+    """search_width * K_max up to 256 (the paper's K_max = 64 with the default
+    width 4): slots, f64 distances and every SearchStats counter equal the oracle."""
+    V, S = ist.gen_synthetic(6_000, 16, "gaussian", rng_seed=8)
+    gi, _ = g.build_index(V, S, g.BuildParams(k_max=kmax, k_local=kmax // 2, bucket_capacity=1000))
+    ox = _oracle_of(gi)
+    Q, _ = ist.gen_synthetic(16, 16, "gaussian", rng_seed=9)
+    for lo, hi in ((-1.0, 2.0), (0.2, 0.5)):
+        p = g.SearchParams(k=10, itopk=96, search_width=width, max_iterations=40)
+        res = g.search_arrays(gi, Q, lo, hi, p, seed_base=5)
+        for i in range(len(Q)):
+            want = beam.beam_search(ox, Q[i], ist.SearchCfg(k=10, lower=lo, upper=hi, itopk=96, search_width=width,
+                                                            max_iterations=40, rng_seed=beam.derive_seed(5, i)))
+            c = int(res.counts[i])
+            assert np.array_equal(res.slots[i, :c], want.slots), (kmax, width, lo, i)
+            got = [int(res.stats[i][f]) for f in STAT_KEYS]
+            assert got == [getattr(want.stats, f) for f in STAT_KEYS], (kmax, width, lo, i)
