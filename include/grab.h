@@ -168,6 +168,15 @@ GRAB_API int grab_bucket_select(const grab_index* h, const double* lower, const 
 GRAB_API int grab_bucket_ids(const grab_index* h, const float* scalars, uint64_t n, int32_t* out,
                     uint32_t mem, void* stream);
 
+/* partition_buckets (layout.py:107-154) on `device`: boundaries (np.unique of the
+ * quantile / width edges) into out_boundaries (host, capacity max_boundaries >=
+ * ceil(n / target_capacity) + 1), *out_m = buckets, and optionally the bucket id
+ * of every scalar into out_ids (mem-space like scalars). Stream: the caller's in
+ * device mode, the legacy default stream otherwise. */
+GRAB_API int grab_partition(int device, const float* scalars, uint64_t n, uint32_t target_capacity, int strategy,
+                            float* out_boundaries, uint32_t max_boundaries, uint32_t* out_m, int32_t* out_ids,
+                            uint32_t mem, void* stream);
+
 /* stateless variants over explicit boundaries f32[m+1] (host pointers) */
 GRAB_API int grab_bucket_ids_raw(const float* boundaries, uint32_t m, const float* scalars, uint64_t n,
                                  int32_t* out);

@@ -87,6 +87,7 @@ _SIGS = {
     "grab_bucket_select": (C.c_int, [P, P, P, u64, P, P, u32, P]),
     "grab_bucket_ids": (C.c_int, [P, P, u64, P, u32, P]),
     "grab_bucket_ids_raw": (C.c_int, [P, u32, P, u64, P]),
+    "grab_partition": (C.c_int, [C.c_int, P, u64, u32, C.c_int, P, u32, C.POINTER(u32), P, u32, P]),
     "grab_bucket_select_raw": (C.c_int, [P, u32, P, P, u64, P, P]),
     "grab_sq_distances": (C.c_int, [P, P, u64, u32, P]),
     "grab_import": (C.c_int, [P, u64, P, P, P, P, u32, P, P, P]),

@@ -247,6 +247,35 @@ def bucket_ids_of(meta, scalars) -> np.ndarray:
     return out
 
 
+def partition_buckets(scalars, target_capacity: int, *, strategy: str = "quantile", capacity: int | None = None,
+                      device: int = 0) -> BucketMeta:
+    """partition_buckets (layout.py:107-154) on the device: quantile (sorted
+    cuts, np.round half-even) or width (f32 linspace) edges, np.unique-collapsed;
+    index_to_bucket sized to ``capacity`` (-1 past n); members in slot order."""
+    if strategy not in _STRATEGY:
+        raise ValueError(f"unknown bucket strategy: {strategy!r}")
+    s = np.ascontiguousarray(np.asarray(scalars, dtype=np.float32).reshape(-1))
+    n = len(s)
+    if n < 1:
+        raise ValueError("cannot partition an empty scalar set")
+    if target_capacity < 1:
+        raise ValueError("target_capacity must be >= 1")
+    cap_b = -(-n // int(target_capacity)) + 1
+    edges = np.empty(max(cap_b, 2), dtype="<f4")
+    m = C.c_uint32(0)
+    ids = np.empty(n, dtype="<i4")
+    L.check(L.lib.grab_partition(int(device), L.ptr(s), n, int(target_capacity), _STRATEGY[strategy], L.ptr(edges),
+                                 len(edges), C.byref(m), L.ptr(ids), L.MEM_HOST, None))
+    mm = int(m.value)
+    cap = n if capacity is None else int(capacity)
+    i2b = np.full(cap, -1, dtype="<i4")
+    i2b[:n] = ids
+    order = np.argsort(ids, kind="stable")
+    cuts = np.searchsorted(ids[order], np.arange(mm + 1))
+    lists = [order[cuts[b]:cuts[b + 1]].tolist() for b in range(mm)]
+    return BucketMeta(boundaries=edges[: mm + 1].copy(), index_to_bucket=i2b, bucket_to_index=lists)
+
+
 def bucket_of(meta, s: float) -> int:
     return int(bucket_ids_of(meta, np.array([s], dtype=np.float32))[0])
 

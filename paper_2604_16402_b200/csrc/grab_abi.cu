@@ -359,6 +359,33 @@ extern "C" int grab_bucket_ids(const grab_index* h, const float* scalars, uint64
   });
 }
 
+extern "C" int grab_partition(int device, const float* scalars, uint64_t n, uint32_t target_capacity, int strategy,
+                              float* out_boundaries, uint32_t max_boundaries, uint32_t* out_m, int32_t* out_ids,
+                              uint32_t mem, void* stream) {
+  return guarded([&] {
+    if (!out_boundaries || !out_m) throw Error(GRAB_ERR_VALUE, "null output");
+    GRAB_CUDA(cudaSetDevice(device));
+    cudaStream_t st = mem == GRAB_MEM_DEVICE ? (cudaStream_t)stream : (cudaStream_t)0;
+    DBuf a, c;
+    const float* s = stage_in(scalars, n, mem, a, st);
+    const std::vector<float> edges = partition_edges_device(s, n, target_capacity, strategy, st);
+    if (edges.size() > max_boundaries) throw Error(GRAB_ERR_VALUE, "boundary buffer too small");
+    std::copy(edges.begin(), edges.end(), out_boundaries);
+    *out_m = (uint32_t)edges.size() - 1;
+    if (out_ids && n) {
+      DBuf db(edges.size() * 4, st);
+      GRAB_CUDA(cudaMemcpyAsync(db.p, edges.data(), edges.size() * 4, cudaMemcpyHostToDevice, st));
+      DevIndex tmp;
+      tmp.bound = db.as<float>();
+      tmp.m = *out_m;
+      int32_t* o = stage_out(out_ids, n, mem, c, st);
+      launch_bucket_ids(tmp, s, n, o, st);
+      copy_back(out_ids, c, n, mem, st);
+      GRAB_CUDA(cudaStreamSynchronize(st));
+    }
+  });
+}
+
 extern "C" int grab_import(grab_index* h, uint64_t n, const float* X, const float* scalars,
                            const uint32_t* adjacency, const float* boundaries, uint32_t m, const int32_t* i2b,
                            const uint32_t* b2i_flat, const uint64_t* b2i_offsets) {

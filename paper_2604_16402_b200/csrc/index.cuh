@@ -104,6 +104,9 @@ void gather_slot_rows(const DevIndex& ix, float* X_out_dev, float* S_out_dev, ui
 
 // ---- bucket lookup (select.cu) ----
 void launch_bucket_ids(const DevIndex& ix, const float* s, uint64_t n, int32_t* out, cudaStream_t st);
+// partition_buckets edges (np.unique applied) for n device scalars (build.cu)
+std::vector<float> partition_edges_device(const float* S, uint64_t n, uint32_t target, int strategy,
+                                          cudaStream_t st);
 void launch_bucket_select(const DevIndex& ix, const double* lo, const double* hi, uint64_t n,
                           int32_t* out_lo, int32_t* out_hi, cudaStream_t st);
 

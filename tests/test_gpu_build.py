@@ -152,3 +152,28 @@ def test_auto_global_pass_follows_reference_limit(g):
     assert rep.global_pass == "exact"  # n <= EXACT_GLOBAL_LIMIT (builder.py:33)
     _, rep = g.build_index(V, S, g.BuildParams(bucket_capacity=1000), global_pass="descent")
     assert rep.global_pass == "descent"
+
+
+def test_partition_buckets_matches_reference_goldens(g, golden):
+    """partition_buckets (layout.py:107-154) on the device: boundaries byte-identical
+    and M_I2B / M_B2I equal to the live reference's on every golden case
+    (quantile, skewed, all-equal, width, ties, odd n)."""
+    gl = golden("layout")
+    cases = {
+        "uniform": (np.random.default_rng(0).random(10_000, dtype=np.float32), 1000, "quantile"),
+        "skewed": ((np.random.default_rng(3).random(5000, dtype=np.float32) ** 8).astype(np.float32), 500, "quantile"),
+        "equal": (np.full(100, 5.0, np.float32), 10, "quantile"),
+        "width": (np.random.default_rng(2).random(1000, dtype=np.float32), 100, "width"),
+        "ties": (np.round(np.random.default_rng(4).random(3000) * 20).astype(np.float32), 97, "quantile"),
+        "odd": (np.random.default_rng(5).standard_normal(1237).astype(np.float32), 100, "quantile"),
+    }
+    for name, (s, cap, strat) in cases.items():
+        meta = g.partition_buckets(s, cap, strategy=strat, capacity=len(s) + 7)
+        assert meta.boundaries.tobytes() == gl[f"{name}_boundaries"].tobytes(), name
+        assert np.array_equal(meta.index_to_bucket[: len(s)], gl[f"{name}_i2b"][: len(s)]), name
+        assert (meta.index_to_bucket[len(s):] == -1).all()
+        flat = [slot for b in meta.bucket_to_index for slot in b]
+        assert sorted(flat) == list(range(len(s))) and all(b == sorted(b) for b in meta.bucket_to_index)
+        assert all(meta.index_to_bucket[x] == bi for bi, b in enumerate(meta.bucket_to_index) for x in b)
+    with pytest.raises(ValueError):
+        g.partition_buckets(np.zeros(0, np.float32), 10)
