@@ -142,6 +142,11 @@ GRAB_API int grab_build_ex(grab_index* h, const float* vectors, const float* sca
 GRAB_API int grab_insert(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids,
                 uint64_t b, uint32_t search_itopk, uint32_t mem, grab_insert_report* report);
 GRAB_API int grab_last_rewired(const grab_index* h, uint32_t* out, uint64_t cap, uint64_t* n_out);
+/* append_batch (layout.py:181-223): rows / scalars / ids and bucket maps only
+ * (adjacency of the new slots stays SENTINEL); [*start, *end) = the new slots.
+ * Needs bucket metadata (a built index). */
+GRAB_API int grab_append(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
+                         uint32_t mem, uint64_t* start, uint64_t* end);
 
 /* ---- search / search_batch (searcher.py:156-248) ----
  * Query i uses range [lower[i*range_stride], upper[i*range_stride]] (stride 0 =

@@ -8,7 +8,8 @@ from .params import (BuildParams, CapacityError, DimensionMismatchError, RangePr
                      VectorRecord)
 from .graph import SENTINEL, BucketMeta, GraphIndex, create_index, from_reference, load_index, save_index
 from .graph import StoreView as VectorStore  # the device-resident store's reference-shaped view
-from .api import (BatchResult, BuildDraft, BuildReport, InsertReport, build_index, insert_batch, select_neighbors,
+from .api import (BatchResult, BuildDraft, BuildReport, InsertReport, append_batch, build_index, insert_batch,
+                  select_neighbors,
                   try_rewire, SearchResult, SearchStats, brute_force_arrays, brute_force_search, bucket_ids_of,
                   bucket_of, intersecting_buckets, partition_buckets, search, search_arrays, search_batch,
                   sq_distance, sq_distances)
@@ -26,5 +27,5 @@ __all__ = [
     "intersecting_buckets", "load_index", "save_index", "search", "search_arrays", "search_batch",
     "sq_distance", "sq_distances", "VectorStore", "partition_buckets", "gen_synthetic", "recall_at_k",
     "FvecsFormatError", "read_fvecs", "read_scalars", "write_fvecs", "write_scalars", "EvalReport",
-    "GroundTruthCache", "SweepSpec", "run_sweep", "scc_count",
+    "GroundTruthCache", "SweepSpec", "run_sweep", "scc_count", "append_batch",
 ]

@@ -82,6 +82,7 @@ _SIGS = {
     "grab_build_ex": (C.c_int, [P, P, P, u64, C.c_int, u32, u32, u32, C.POINTER(BuildReportC), P]),
     "grab_insert": (C.c_int, [P, P, P, P, u64, u32, u32, C.POINTER(InsertReportC)]),
     "grab_last_rewired": (C.c_int, [P, P, u64, C.POINTER(u64)]),
+    "grab_append": (C.c_int, [P, P, P, P, u64, u32, C.POINTER(u64), C.POINTER(u64)]),
     "grab_search": (C.c_int, [P, P, u64, P, P, u64, C.POINTER(SearchParamsC), P, u64, u64, u64, P, P, P, P, u32, P]),
     "grab_brute_force": (C.c_int, [P, P, u64, P, P, u64, u32, u64, P, P, P, u32, P]),
     "grab_bucket_select": (C.c_int, [P, P, P, u64, P, P, u32, P]),

@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib as L
-from .graph import BucketMeta, GraphIndex, create_index
+from .graph import BucketMeta, GraphIndex, StoreView, create_index
 from .params import BuildParams, DimensionMismatchError, RangePredicate, SearchParams
 
 
@@ -465,6 +465,35 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
                         evictions_redundant=int(rep.evictions_redundant), forced_links=int(rep.forced_links),
                         rewired_rows=rw.astype(np.int64).tolist(), wall_time_s=float(rep.wall_time_s),
                         phase_seconds={k: float(rep.phase_seconds[i]) for i, k in enumerate(_INSERT_PHASES)})
+
+
+def append_batch(index: GraphIndex, vectors, scalars, ids=None) -> tuple[int, int]:
+    """append_batch (layout.py:181-223) on the device index: rows, scalars, ids and
+    bucket maps at the tail, adjacency of the new slots left SENTINEL (no edges);
+    returns [start, end). The reference takes (store, meta, ...); here the index
+    owns both. Needs a built index (bucket metadata)."""
+    if isinstance(index, StoreView):
+        index = index._ix
+    V = np.asarray(vectors, dtype=np.float32)
+    S = np.ascontiguousarray(np.asarray(scalars, dtype=np.float32).reshape(-1))
+    b = len(V)
+    if b == 0:
+        c = index.count
+        return c, c
+    if V.ndim != 2 or V.shape[1] != index.dim:
+        raise DimensionMismatchError(f"vectors have shape {tuple(V.shape)}, index dimension is {index.dim}")
+    if len(S) != b:
+        raise ValueError(f"{b} vectors but {len(S)} scalars")
+    if not np.all(np.isfinite(S)):
+        raise ValueError("scalars must be finite")
+    V = np.ascontiguousarray(V)
+    Ih = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+    st, en = C.c_uint64(0), C.c_uint64(0)
+    L.check(L.lib.grab_append(index.handle, L.ptr(V), L.ptr(S), L.ptr(Ih), b, L.MEM_HOST, C.byref(st), C.byref(en)))
+    start, end = int(st.value), int(en.value)
+    index._ids[start:end] = np.arange(start, end) if Ih is None else Ih
+    index._touch()
+    return start, end
 
 
 def _rows_of(store) -> np.ndarray:

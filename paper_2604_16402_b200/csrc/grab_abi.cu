@@ -532,6 +532,19 @@ extern "C" int grab_insert(grab_index* h, const float* vectors, const float* sca
   });
 }
 
+extern "C" int grab_append(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
+                           uint32_t mem, uint64_t* start, uint64_t* end) {
+  return guarded([&] {
+    check_handle(h);
+    std::lock_guard<std::mutex> lk(h->writer);
+    DevIndex& ix = h->ix;
+    set_device(ix);
+    ix.adj_version++;
+    append_batch_device(ix, vectors, scalars, ids, b, mem, start, end);
+    ix.adj_version++;
+  });
+}
+
 extern "C" int grab_last_rewired(const grab_index* h, uint32_t* out, uint64_t cap, uint64_t* n_out) {
   return guarded([&] {
     check_handle(h);

@@ -95,6 +95,8 @@ void layout_from_slots(DevIndex& ix, const float* X_slot, const float* S_slot, u
                        const std::vector<uint32_t>& bucket_sizes);
 // Append `b` fresh slots [start, start+b) (bucket ids already in ix.i2b) to
 // their slabs, relayouting all slabs when one overflows.
+void append_batch_device(DevIndex& ix, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
+                         uint32_t mem, uint64_t* start_out, uint64_t* end_out);
 void layout_append(DevIndex& ix, const float* X_new, const float* S_new, uint64_t start, uint64_t b);
 void upload_bucket_tables(DevIndex& ix);
 // slot-space adjacency -> phys-space (import) and back (export)

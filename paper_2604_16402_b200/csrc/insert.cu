@@ -690,6 +690,39 @@ __global__ void k_fresh_phys(const uint32_t* s2p, uint64_t start, uint64_t b, ui
   if (i < b) out[i] = s2p[start + i];
 }
 
+// append_batch (layout.py:181-223) alone: rows, scalars, ids and bucket maps at
+// the tail (zero-shift slab placement), adjacency left SENTINEL; [start, end).
+void append_batch_device(DevIndex& ix, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
+                         uint32_t mem, uint64_t* start_out, uint64_t* end_out) {
+  cudaStream_t st = ix.stream;
+  const uint64_t n0 = ix.count;
+  if (start_out) *start_out = n0;
+  if (end_out) *end_out = n0;
+  if (b == 0) return;
+  if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no bucket metadata (build it first)");
+  if (n0 + b > ix.n_cap)
+    throw Error(GRAB_ERR_CAPACITY, "capacity exhausted: " + std::to_string(n0) + " claimed + " + std::to_string(b) +
+                                       " requested > " + std::to_string(ix.n_cap));
+  Pool pool(st);
+  const float* Vd = vectors;
+  const float* Sd = scalars;
+  if (mem == GRAB_MEM_HOST) {
+    for (uint64_t i = 0; i < b; ++i)
+      if (!std::isfinite(scalars[i])) throw Error(GRAB_ERR_VALUE, "scalars must be finite");
+    float* v = pool.alloc<float>(b * ix.dim);
+    float* sc = pool.alloc<float>(b);
+    GRAB_CUDA(cudaMemcpyAsync(v, vectors, b * ix.dim * 4, cudaMemcpyHostToDevice, st));
+    GRAB_CUDA(cudaMemcpyAsync(sc, scalars, b * 4, cudaMemcpyHostToDevice, st));
+    Vd = v;
+    Sd = sc;
+  }
+  launch_bucket_ids(ix, Sd, b, ix.i2b + n0, st);
+  layout_append(ix, Vd, Sd, n0, b);
+  for (uint64_t i = 0; i < b; ++i) ix.ids[n0 + i] = ids ? ids[i] : (int64_t)(n0 + i);
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  if (end_out) *end_out = n0 + b;
+}
+
 void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
                          uint32_t search_itopk, uint32_t mem, grab_insert_report* rep) {
   const double t_begin = now_s();

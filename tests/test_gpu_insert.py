@@ -218,3 +218,30 @@ def test_insert_kmax64_matches_oracle(g):
     assert [getattr(rep, k) for k in KEYS] == [getattr(t, k) for k in KEYS]
     assert rep.rewired_rows == t.rewired_rows
     assert np.array_equal(gi.adjacency[:4_400], ref.adjacency[:4_400])
+
+
+def test_append_batch_matches_oracle(g):
+    """append_batch (layout.py:181-223): slots, rows, scalars, ids and the bucket
+    maps equal the oracle's append; new adjacency rows stay SENTINEL; the
+    capacity and dimension errors map to the reference's classes."""
+    X, S = ist.gen_lowrank(2_300, 16, seed=21)
+    cfg = ist.BuildCfg(k_max=16, k_local=8, bucket_capacity=500)
+    ref, _, _ = construct.build(X[:2_000], S[:2_000], cfg, capacity=2_400)
+    gi = g.load_index(ist.container_bytes(ref), g.BuildParams(k_max=16, k_local=8, bucket_capacity=500))
+    ids = np.arange(9_000, 9_300, dtype=np.int64)
+    assert g.append_batch(gi, X[2_000:], S[2_000:], ids=ids) == (2_000, 2_300)
+    assert ist.append_rows(ref, X[2_000:], S[2_000:], ids=ids) == (2_000, 2_300)
+    assert gi.count == 2_300 and np.array_equal(gi.store.ids[2_000:2_300], ids)
+    assert np.array_equal(gi.store.X[:2_300], ref.X[:2_300]) and np.array_equal(gi.store.scalars[:2_300],
+                                                                             ref.scalars[:2_300])
+    assert np.array_equal(gi.meta.index_to_bucket[:2_300], ref.i2b[:2_300])
+    assert [list(b) for b in gi.meta.bucket_to_index] == [list(b) for b in ref.b2i]
+    assert (gi.adjacency[2_000:2_300] == SENT).all()
+    assert np.array_equal(gi.adjacency[:2_000], ref.adjacency[:2_000])
+    with pytest.raises(g.CapacityError):
+        g.append_batch(gi, X[:200], S[:200])
+    with pytest.raises(g.DimensionMismatchError):
+        g.append_batch(gi, np.zeros((3, 8), np.float32), np.zeros(3, np.float32))
+    # a graph-less append followed by a search: the appended rows are reachable only as seeds
+    r = g.search_arrays(gi, X[2_100:2_110], 0.0, 1.0, g.SearchParams(k=10, itopk=64), seed_base=1)
+    assert (r.counts == 10).all()
