@@ -140,15 +140,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_knn_screen_tc(const __grid_constant__ CUtensorMap tmap_ahi, const __grid_constant__ CUtensorMap tmap_alo,
                     const __grid_constant__ CUtensorMap tmap_bhi, const __grid_constant__ CUtensorMap tmap_blo,
                     const KnnJob* jobs, const Attr* attr, const float* row_norms, const float* norms,
-                    uint32_t nkc, uint32_t KP, uint32_t* cand, int causal, uint32_t STAGES, uint32_t NG) {
+                    uint32_t nkc, uint32_t KP, uint32_t* cand, int causal, uint32_t STAGES, uint32_t NG,
+                    int stream_a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t a_bytes = nkc * Smem::kChunkA;  // per hi / lo
-  const uint32_t b_bytes = nkc * Smem::kChunkB;
+  // resident A (d <= 128): A hi/lo for every K chunk loaded once, the ring holds
+  // one column tile's B hi/lo (all K chunks) per stage. Streamed A (d > 128):
+  // every ring stage holds ONE K chunk of A hi/lo and B hi/lo, so any d fits and
+  // the accumulator sums the chunks in TMEM.
+  const uint32_t a_bytes = stream_a ? 0u : nkc * Smem::kChunkA;  // resident A per hi / lo
+  const uint32_t b_bytes = stream_a ? 0u : nkc * Smem::kChunkB;
+  const uint32_t st_bytes = stream_a ? 2 * (Smem::kChunkA + Smem::kChunkB) : 2 * b_bytes;  // one ring stage
   uint8_t* A_hi = smem;
   uint8_t* A_lo = A_hi + a_bytes;
-  uint8_t* B = A_lo + a_bytes;  // STAGES x (hi, lo)
-  uint64_t* H = (uint64_t*)(B + STAGES * 2 * b_bytes);  // NG column groups x [KP][BM]
+  uint8_t* B = A_lo + a_bytes;  // STAGES x stage
+  uint64_t* H = (uint64_t*)(B + STAGES * st_bytes);  // NG column groups x [KP][BM]
   uint64_t* bars = H + NG * BM * KP;
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
@@ -185,7 +191,54 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 && stream_a) {
+    if (lane == 0) {
+      // ---- TMA producer, streamed A: ring slot u = (tile t, K chunk c)
+      uint32_t u = 0;
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const int32_t row = (int32_t)(job.c0 + t * BN);
+        for (uint32_t c = 0; c < nkc; ++c, ++u) {
+          const uint32_t s = u % STAGES, round = u / STAGES;
+          mbar_wait(b_empty + s, (round & 1) ^ 1);
+          uint8_t* ah = B + s * st_bytes;
+          uint8_t* al = ah + Smem::kChunkA;
+          uint8_t* bh = al + Smem::kChunkA;
+          uint8_t* bl = bh + Smem::kChunkB;
+          mbar_expect_tx(b_full + s, st_bytes);
+          tma_load_2d(ah, &tmap_ahi, b_full + s, (int32_t)(c * KCH), (int32_t)job.r0);
+          tma_load_2d(al, &tmap_alo, b_full + s, (int32_t)(c * KCH), (int32_t)job.r0);
+          tma_load_2d(bh, &tmap_bhi, b_full + s, (int32_t)(c * KCH), row);
+          tma_load_2d(bl, &tmap_blo, b_full + s, (int32_t)(c * KCH), row);
+        }
+      }
+    }
+  } else if (warp == 1 && stream_a) {
+    if (lane == 0) {
+      // ---- UMMA issuer, streamed A: one commit per K chunk frees its ring slot
+      uint32_t u = 0;
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t as = t & 1, around = t >> 1;
+        mbar_wait(acc_empty + as, (around & 1) ^ 1);
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (uint32_t c = 0; c < nkc; ++c, ++u) {
+          const uint32_t s = u % STAGES, round = u / STAGES;
+          mbar_wait(b_full + s, round & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t ah = smem_u32(B + s * st_bytes), al = ah + Smem::kChunkA;
+          const uint32_t bh = al + Smem::kChunkA, bl = bh + Smem::kChunkB;
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {
+            const uint32_t off = kk * 32;
+            umma_bf16(d_tmem, smem_desc(ah + off), smem_desc(bh + off), (c | kk) != 0u);
+            umma_bf16(d_tmem, smem_desc(ah + off), smem_desc(bl + off), 1);
+            umma_bf16(d_tmem, smem_desc(al + off), smem_desc(bh + off), 1);
+          }
+          umma_commit(b_empty + s);
+        }
+        umma_commit(acc_full + as);
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer
       mbar_expect_tx(a_full, 2 * a_bytes);
@@ -398,8 +451,8 @@ static CUtensorMap make_map(void* base, uint64_t rows, uint32_t kp, uint32_t box
 
 bool knn_tc_supported(const DevIndex& ix, uint32_t KP) {
   if (getenv("GRAB_KNN_SIMT")) return false;
-  const uint32_t kp = (ix.dp + tc::KCH - 1) / tc::KCH * tc::KCH;
-  return kp <= 128 && KP <= tc::KP_MAX;
+  (void)ix;  // any d: rows wider than 128 stream A through the ring
+  return KP <= tc::KP_MAX;
 }
 
 void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, uint32_t njobs, uint32_t KP,
@@ -422,12 +475,14 @@ void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, 
   const CUtensorMap ahi = make_map(hi, rows, kp, BM), alo = make_map(lo, rows, kp, BM);
   const CUtensorMap bhi = make_map(hi, rows, kp, BN), blo = make_map(lo, rows, kp, BN);
   // prefer two epilogue column groups (8 epilogue warps), then the deepest B ring that fits
+  const int stream_a = kp > 128 ? 1 : 0;
   uint32_t stages = 0, ng = 0;
   size_t smem = 0;
   for (uint32_t g = 2; g >= 1 && !stages; --g) {
     for (uint32_t s = MAX_STAGES; s >= 2; --s) {
-      const size_t b = 1024 + 2 * (size_t)nkc * BM * 128 + s * 2 * (size_t)nkc * BN * 128 +
-                       (size_t)g * BM * KP * 8 + 16 * 8;
+      const size_t ring = stream_a ? s * 2 * (size_t)(Smem::kChunkA + Smem::kChunkB)
+                                   : 2 * (size_t)nkc * BM * 128 + s * 2 * (size_t)nkc * BN * 128;
+      const size_t b = 1024 + ring + (size_t)g * BM * KP * 8 + 16 * 8;
       if (b <= 227 * 1024) {
         stages = s;
         ng = g;
@@ -439,7 +494,7 @@ void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, 
   if (!stages) throw Error(GRAB_ERR_VALUE, "tensor-core kNN tile exceeds shared memory");
   GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_knn_screen_tc<<<njobs, kThreads, smem, st>>>(ahi, alo, bhi, blo, djobs, ix.attr, norms, nm, nkc, KP, cand,
-                                                 causal ? 1 : 0, stages, ng);
+                                                 causal ? 1 : 0, stages, ng, stream_a);
   GRAB_CHECK_LAUNCH();
   GRAB_CUDA(cudaFreeAsync(nm, st));
   GRAB_CUDA(cudaFreeAsync(hi, st));

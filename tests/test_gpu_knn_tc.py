@@ -20,8 +20,9 @@ def f64_knn(X, k):
     return np.array([np.lexsort((np.arange(n), d[i]))[: min(k, n - 1)] for i in range(n)])
 
 
-@pytest.mark.parametrize("d", [8, 16, 96, 128])
+@pytest.mark.parametrize("d", [8, 16, 96, 128, 200, 384, 960])
 def test_tc_pass1_equals_f64_oracle(d):
+    """d > 128 streams A through the ring one K chunk at a time (TMEM accumulates)."""
     import paper_2604_16402_b200 as g
     r = np.random.default_rng(7 + d)
     V = r.standard_normal((700, d)).astype(np.float32)
@@ -32,17 +33,17 @@ def test_tc_pass1_equals_f64_oracle(d):
     assert np.array_equal(dr.global_rows[:, :1].astype(np.int64), want[:, :1])
 
 
-def _build_draft(env_simt: bool, seed: int):
+def _build_draft(env_simt: bool, seed: int, dim: int = 128):
     code = f"""
 import sys, numpy as np
 sys.path.insert(0, {ROOT!r})
 import paper_2604_16402_b200 as g
 from oracle import index_state as ist
-X, S = ist.gen_lowrank(30000, 128, seed={seed})
+X, S = ist.gen_lowrank(30000, {dim}, seed={seed})
 gi, rep, dr = g.build_index(X, S, g.BuildParams(k_max=32, k_local=16, bucket_capacity=3000), return_draft=True)
 np.savez(sys.argv[1], f=dr.forward_rows, m=dr.rows, g=dr.global_rows, a=gi.adjacency[:gi.count])
 """
-    out = f"/tmp/draft_{int(env_simt)}_{seed}.npz"
+    out = f"/tmp/draft_{int(env_simt)}_{seed}_{dim}.npz"
     env = dict(os.environ)
     if env_simt:
         env["GRAB_KNN_SIMT"] = "1"
@@ -52,9 +53,10 @@ np.savez(sys.argv[1], f=dr.forward_rows, m=dr.rows, g=dr.global_rows, a=gi.adjac
     return np.load(out)
 
 
-def test_tc_build_matches_simt_build():
-    a = _build_draft(False, 5)
-    b = _build_draft(True, 5)
+@pytest.mark.parametrize("dim", [128, 960])
+def test_tc_build_matches_simt_build(dim):
+    a = _build_draft(False, 5, dim)
+    b = _build_draft(True, 5, dim)
     for key in ("f", "g", "m", "a"):
         same = np.mean([np.array_equal(x, y) for x, y in zip(a[key], b[key])])
         print(key, same)
