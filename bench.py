@@ -374,7 +374,11 @@ def run_sharded(args, cfg, rank, world, local, dist):
                        "exchange": ("peer-memory stores (CUDA IPC over NVLink)" if args.exchange == "p2p"
                                     else "NCCL all_to_all_single") if dist else "none (1 shard)",
                        "global_pass": brep.global_pass},
-            "build_s": round(build_s, 3), "gpu_launches": None, "clocks": clk.summary()}
+            # rank 0, per step: search grid + retry grid, the exchange's pack kernels
+            # (p2p: fill + pack; NCCL: pack, its collective kernels not counted), top-k merge
+            "build_s": round(build_s, 3),
+            "gpu_launches": args.steps * (2 + (2 if args.exchange == "p2p" else 1) + 1),
+            "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line))
     if dist:
