@@ -20,21 +20,25 @@ constexpr uint32_t kScreenTileBytes =
 
 // Max-heap (h[0] largest) of one row, element i at h[i * BM]: rows are
 // interleaved so neighbouring threads hit neighbouring banks.
+// 4-ary (like the tcgen05 screen's): half the dependent load levels of a binary heap
 __device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t n, uint64_t key) {
   uint32_t i = 0;
   while (true) {
-    uint32_t l = 2 * i + 1, r = l + 1, big = i;
-    uint64_t kb = key;
-    if (l < n && h[l * BM] > kb) {
-      big = l;
-      kb = h[l * BM];
+    const uint32_t c0 = 4 * i + 1;
+    if (c0 >= n) break;
+    uint64_t kb = h[c0 * BM];
+    uint32_t big = c0;
+#pragma unroll
+    for (uint32_t j = 1; j < 4; ++j) {
+      const uint32_t c = c0 + j;
+      const uint64_t v = c < n ? h[c * BM] : 0ull;
+      if (v > kb) {
+        kb = v;
+        big = c;
+      }
     }
-    if (r < n && h[r * BM] > kb) {
-      big = r;
-      kb = h[r * BM];
-    }
-    if (big == i) break;
-    h[i * BM] = h[big * BM];
+    if (kb <= key) break;
+    h[i * BM] = kb;
     i = big;
   }
   h[i * BM] = key;

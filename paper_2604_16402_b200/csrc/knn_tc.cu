@@ -108,21 +108,31 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 
 // Max-heap of n keys for one row, element i at h[i * BM] (rows interleaved so
 // the 32 lanes of a warp touch 32 consecutive words: no bank conflicts).
+// HEAP_ARY-ary (4): half the levels of a binary heap, and a level's child loads
+// are independent, so the sift-down's chain of dependent shared loads halves
+// (screen 47 -> 38 ms at cfg2 pass 1)
+#ifndef GRAB_HEAP_ARY
+#define GRAB_HEAP_ARY 4
+#endif
 __device__ __forceinline__ void heap_replace_top(uint64_t* h, uint32_t n, uint64_t key) {
+  constexpr uint32_t A = GRAB_HEAP_ARY;
   uint32_t i = 0;
   while (true) {
-    uint32_t l = 2 * i + 1, r = l + 1, big = i;
-    uint64_t kb = key;
-    if (l < n && h[l * BM] > kb) {
-      big = l;
-      kb = h[l * BM];
+    const uint32_t c0 = A * i + 1;
+    if (c0 >= n) break;
+    uint64_t kb = h[c0 * BM];
+    uint32_t big = c0;
+#pragma unroll
+    for (uint32_t j = 1; j < A; ++j) {
+      const uint32_t c = c0 + j;
+      const uint64_t v = c < n ? h[c * BM] : 0ull;
+      if (v > kb) {
+        kb = v;
+        big = c;
+      }
     }
-    if (r < n && h[r * BM] > kb) {
-      big = r;
-      kb = h[r * BM];
-    }
-    if (big == i) break;
-    h[i * BM] = h[big * BM];
+    if (kb <= key) break;
+    h[i * BM] = kb;
     i = big;
   }
   h[i * BM] = key;
