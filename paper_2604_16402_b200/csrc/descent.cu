@@ -221,25 +221,31 @@ __global__ void k_count_dst(const uint32_t* dst, uint64_t nk, uint32_t n, uint32
   if (e < nk && dst[e] < n) atomicAdd(cnt + dst[e], 1u);
 }
 
-// joint[v] = [graph[v] (k) | nearest k reverse sources (-1 padded)]
-__global__ void k_joint(const int32_t* graph, uint32_t n, uint32_t k, const uint32_t* sdst, const uint64_t* skey,
-                        const uint32_t* off, uint64_t nk, int32_t* joint) {
+// joint[v] = [graph[v] (k) | nearest k reverse sources (-1 padded)], and
+// jd[v] = their distances to v, already known: the forward ones from the
+// current graph, the reverse ones from the reverse keys -- bit-identical to a
+// recomputation (same lane-group order; (a-b)^2 == (b-a)^2 in f64)
+__global__ void k_joint(const int32_t* graph, const float* dist, uint32_t n, uint32_t k, int32_t* joint, float* jd) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i < (uint64_t)n * k) {
     const uint64_t v = i / k, j = i % k;
     joint[v * 2 * k + j] = graph[i];
     joint[v * 2 * k + k + j] = -1;
+    jd[v * 2 * k + j] = dist[i];
   }
 }
 
 __global__ void k_joint_rev(uint32_t n, uint32_t k, const uint32_t* sdst, const uint64_t* skey, const uint32_t* off,
-                            uint64_t nk, int32_t* joint) {
+                            uint64_t nk, int32_t* joint, float* jd) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= nk) return;
   const uint32_t v = sdst[i];
   if (v >= n) return;
   const uint64_t pos = i - off[v];
-  if (pos < k) joint[(uint64_t)v * 2 * k + k + pos] = (int32_t)(uint32_t)skey[i];
+  if (pos < k) {
+    joint[(uint64_t)v * 2 * k + k + pos] = (int32_t)(uint32_t)skey[i];
+    jd[(uint64_t)v * 2 * k + k + pos] = __uint_as_float((uint32_t)(skey[i] >> 32));
+  }
 }
 
 // Key of a (dist, column) candidate as one u64: f32 bits above the column.
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, cons
                                                       uint32_t k, const uint32_t* hop, uint32_t nhop,
                                                       const uint32_t* s2p, const Attr* attr, const float* X,
                                                       uint32_t dp, uint32_t C, uint32_t H, int32_t* out_graph,
-                                                      float* out_dist) {
+                                                      float* out_dist, const float* jd) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
   const uint32_t v = blockIdx.x * WPB + wib;
@@ -318,6 +324,27 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, cons
   uint64_t best = ~0ull;  // lanes >= k never receive real entries
   for (uint32_t c0 = 0; c0 < C; c0 += 32) {
     const uint32_t flags = fl[c0 >> 5];
+    if (c0 + 32 <= J) {
+      // own joint row: every distance is known (no row loads)
+      const uint32_t c = c0 + lane;
+      uint64_t key = dc_key(((flags >> lane) & 1u) ? jd[(uint64_t)v * J + c] : kInfF, c);
+      const uint64_t tail = __shfl_sync(0xFFFFFFFFu, best, k - 1);
+      if (!__any_sync(0xFFFFFFFFu, key < tail)) continue;
+      for (uint32_t kk = 2; kk <= 32; kk <<= 1)
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+          const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, key, j);
+          const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
+          if ((lower == up) ? (o < key) : (o > key)) key = o;
+        }
+      const uint64_t rev = __shfl_sync(0xFFFFFFFFu, key, 31 - lane);
+      best = rev < best ? rev : best;
+      for (uint32_t j = 16; j > 0; j >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, best, j);
+        const bool lower = (lane & j) == 0;
+        if (lower ? (o < best) : (o > best)) best = o;
+      }
+      continue;
+    }
     double sums[8];
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -481,6 +508,7 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   if (C >= 65535 || H > 65536) throw Error(GRAB_ERR_VALUE, "descent candidate set too large");
   int32_t* joint = S.alloc<int32_t>((uint64_t)n * J);
   int32_t* jointp = S.alloc<int32_t>((uint64_t)n * J);
+  float* jd = S.alloc<float>((uint64_t)n * J);
   int32_t* g2 = S.alloc<int32_t>(nk);
   float* d2 = S.alloc<float>(nk);
   uint64_t* key2 = S.alloc<uint64_t>(nk);
@@ -512,9 +540,9 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
     k_count_dst<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(dsts, nk, n, cnt);
     GRAB_CHECK_LAUNCH();
     exclusive_scan_u32(cnt, off, n + 1, st);
-    k_joint<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(graph, n, k, dsts, key2t, off, nk, joint);
+    k_joint<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(graph, dist, n, k, joint, jd);
     GRAB_CHECK_LAUNCH();
-    k_joint_rev<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(n, k, dsts, key2t, off, nk, joint);
+    k_joint_rev<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(n, k, dsts, key2t, off, nk, joint, jd);
     GRAB_CHECK_LAUNCH();
     const std::vector<uint32_t> perm = hg.permutation(J);
     GRAB_CUDA(cudaMemcpyAsync(dhop, perm.data(), nhop * 4, cudaMemcpyHostToDevice, st));
@@ -522,7 +550,7 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
     GRAB_CHECK_LAUNCH();
     k_descent<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem, st>>>(joint, jointp, n, k, dhop, nhop, ix.slot2phys,
                                                                      ix.attr, ix.X,
-                                                                     ix.dp, C, H, g2, d2);
+                                                                     ix.dp, C, H, g2, d2, jd);
     GRAB_CHECK_LAUNCH();
     std::swap(graph, g2);
     std::swap(dist, d2);
