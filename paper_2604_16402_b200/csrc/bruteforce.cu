@@ -172,8 +172,10 @@ void run_bruteforce(const DevIndex& ix, const float* Q, uint64_t nq, const doubl
     go(k_bruteforce<4>);
   else if (nc <= 8)
     go(k_bruteforce<8>);
+  else if (nc <= 16)
+    go(k_bruteforce<16>);
   else
-    throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported");
+    throw Error(GRAB_ERR_VALUE, "dimension > 2048 not supported");
 }
 
 }  // namespace grab
@@ -208,8 +210,10 @@ void run_sq_distances(const float* q, const float* rows, uint64_t n, uint32_t dp
     k_sq_distances<4><<<blocks, 128, 0, st>>>(q, rows, n, dp, out);
   else if (nc <= 8)
     k_sq_distances<8><<<blocks, 128, 0, st>>>(q, rows, n, dp, out);
+  else if (nc <= 16)
+    k_sq_distances<16><<<blocks, 128, 0, st>>>(q, rows, n, dp, out);
   else
-    throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported");
+    throw Error(GRAB_ERR_VALUE, "dimension > 2048 not supported");
   GRAB_CHECK_LAUNCH();
 }
 

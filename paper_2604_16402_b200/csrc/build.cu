@@ -519,8 +519,10 @@ static void launch_repair(const DevIndex& ix, const uint32_t* orph, uint32_t n, 
     k_repair<2><<<1, 32, 0, st>>>(orph, n, ix.adj, K, kl, indeg, ix.X, ix.dp, added);
   else if (nc <= 4)
     k_repair<4><<<1, 32, 0, st>>>(orph, n, ix.adj, K, kl, indeg, ix.X, ix.dp, added);
-  else
+  else if (nc <= 8)
     k_repair<8><<<1, 32, 0, st>>>(orph, n, ix.adj, K, kl, indeg, ix.X, ix.dp, added);
+  else
+    k_repair<16><<<1, 32, 0, st>>>(orph, n, ix.adj, K, kl, indeg, ix.X, ix.dp, added);
   GRAB_CHECK_LAUNCH();
 }
 

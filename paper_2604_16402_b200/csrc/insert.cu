@@ -80,8 +80,8 @@ __device__ __forceinline__ double row_dist(const RowRegs<NC>& q, const float* X,
 // distance of row g lands on lanes with lane >> SH == g.
 template <int NC>
 struct Batch {
-  static constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : 2);
-  static constexpr int SH = G == 8 ? 2 : (G == 4 ? 3 : 4);
+  static constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : (NC <= 8 ? 2 : 1));
+  static constexpr int SH = G == 8 ? 2 : (G == 4 ? 3 : (G == 2 ? 4 : 5));
 };
 
 // Distances from `r` to rows p[0..G) (ok[g] false: row not read, partial 0);
@@ -681,8 +681,10 @@ static void by_nc(uint32_t dp, F&& f) {
     f(std::integral_constant<int, 4>{});
   else if (nc <= 8)
     f(std::integral_constant<int, 8>{});
+  else if (nc <= 16)
+    f(std::integral_constant<int, 16>{});
   else
-    throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported");
+    throw Error(GRAB_ERR_VALUE, "dimension > 2048 not supported");
 }
 
 __global__ void k_fresh_phys(const uint32_t* s2p, uint64_t start, uint64_t b, uint32_t* out) {

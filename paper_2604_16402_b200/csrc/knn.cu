@@ -268,8 +268,10 @@ void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob
     go(k_knn_rerank<4>);
   else if (nc <= 8)
     go(k_knn_rerank<8>);
+  else if (nc <= 16)
+    go(k_knn_rerank<16>);
   else
-    throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported");
+    throw Error(GRAB_ERR_VALUE, "dimension > 2048 not supported");
   GRAB_CUDA(cudaStreamSynchronize(st));
   if (dbg) {
     const double t2 = clk();

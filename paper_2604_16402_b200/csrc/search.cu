@@ -525,7 +525,8 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
 #define GRAB_SEARCH_MINB 6
 #endif
 template <int NC, int EPL, bool FULL>
-__global__ void __launch_bounds__(128, EPL >= 8 ? 4 : GRAB_SEARCH_MINB) k_search(SearchArgs a, SearchShape sh) {
+__global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARCH_MINB))
+    k_search(SearchArgs a, SearchShape sh) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t lt = (1u << lane) - 1;
@@ -829,7 +830,7 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
                        uint32_t dp) {
   SearchShape s;
   const uint32_t nc = (dp + 127) / 128;
-  s.qbytes = nc > 2 ? (nc <= 4 ? 4u : 8u) * 512u : 0u;  // QueryRegs<NC>::kShared staging
+  s.qbytes = nc > 2 ? (nc <= 4 ? 4u : nc <= 8 ? 8u : 16u) * 512u : 0u;  // QueryRegs<NC>::kShared staging
   s.itopk = itopk;
   s.width = width;
   const uint32_t fan = width * k_max;
@@ -869,6 +870,7 @@ static void with_kernel(uint32_t nc, uint32_t epl, bool full, F&& f) {
   GRAB_K(1, 1) GRAB_K(1, 2) GRAB_K(1, 4) GRAB_K(2, 1) GRAB_K(2, 2) GRAB_K(2, 4)
   GRAB_K(4, 1) GRAB_K(4, 2) GRAB_K(4, 4) GRAB_K(8, 1) GRAB_K(8, 2) GRAB_K(8, 4)
   GRAB_K(1, 8) GRAB_K(2, 8) GRAB_K(4, 8) GRAB_K(8, 8)  // width * K_max up to 256 (e.g. K_max 64, width 4)
+  GRAB_K(16, 1) GRAB_K(16, 2) GRAB_K(16, 4) GRAB_K(16, 8)  // 1024 < d <= 2048
 #undef GRAB_K
   throw Error(GRAB_ERR_VALUE, "unsupported search kernel shape");
 }
@@ -882,8 +884,8 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   const uint32_t smem = lay.bytes * wpb;
   if (smem > 227 * 1024) throw Error(GRAB_ERR_VALUE, "search parameters exceed shared memory (itopk too large)");
   uint32_t nc = (uint32_t)div_up(a.dp, 128);
-  nc = nc <= 1 ? 1 : nc <= 2 ? 2 : nc <= 4 ? 4 : nc <= 8 ? 8 : 0;
-  if (!nc) throw Error(GRAB_ERR_VALUE, "dimension > 1024 not supported by the search kernel");
+  nc = nc <= 1 ? 1 : nc <= 2 ? 2 : nc <= 4 ? 4 : nc <= 8 ? 8 : nc <= 16 ? 16 : 0;
+  if (!nc) throw Error(GRAB_ERR_VALUE, "dimension > 2048 not supported by the search kernel");
   uint32_t epl = (uint32_t)div_up(sh.width * a.k_max, 32);
   epl = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
   if (epl > 8 || sh.cmax > 256) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 256 not supported");
