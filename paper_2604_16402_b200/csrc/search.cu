@@ -549,7 +549,13 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
   const uint32_t kshift = (K & (K - 1)) == 0 ? 31 - __clz(K) : 0;  // power-of-two K: shifts, not divisions
   const uint32_t nwork = a.nwork_dev ? *a.nwork_dev : a.nwork;
 
-  for (uint32_t item = gw; item < nwork; item += nw) {
+  auto next_item = [&](uint32_t cur) -> uint32_t {
+    if (!a.work_ctr) return cur + nw;
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(a.work_ctr, 1u);
+    return __shfl_sync(kFull, it, 0);
+  };
+  for (uint32_t item = a.work_ctr ? next_item(0) : gw; item < nwork; item = next_item(item)) {
     const uint32_t qi = a.qmap ? a.qmap[item] : item;
     const float lo_f = __double2float_rn(a.lower[(uint64_t)qi * a.range_stride]);
     const float hi_f = __double2float_rn(a.upper[(uint64_t)qi * a.range_stride]);
@@ -937,7 +943,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
 // order makes the reuse safe without host synchronization).
 struct SearchWs {
   std::mutex mu;  // host-side: one enqueue at a time per stream (threads may share a stream)
-  DBufLite tables, big_tables, ovf;
+  DBufLite tables, big_tables, ovf, ctr;
 };
 struct SearchWsCache {
   std::mutex mu;
@@ -980,6 +986,10 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   ovfb.ensure((a.nwork + 1) * sizeof(uint32_t), st);
   uint32_t* ovf = (uint32_t*)ovfb.p;
   GRAB_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
+  ws.ctr.ensure(2 * sizeof(uint32_t), st);
+  uint32_t* ctr = (uint32_t*)ws.ctr.p;
+  GRAB_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(uint32_t), st));
+  a.work_ctr = getenv("GRAB_STATIC_WORK") ? nullptr : ctr;
   a.ovf_count = ovf;
   a.ovf_list = ovf + 1;
   a.qmap = nullptr;
@@ -991,6 +1001,7 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   b.nwork_dev = ovf;
   b.ovf_count = nullptr;  // cannot overflow: the table bounds every insert of max_iter iterations
   b.ovf_list = nullptr;
+  b.work_ctr = a.work_ctr ? ctr + 1 : nullptr;
   launch(b, big, ix.num_sms, st, big_tables, (uint64_t)ix.num_sms);
   if (getenv("GRAB_DEBUG")) {
     uint32_t n_ovf = 0;

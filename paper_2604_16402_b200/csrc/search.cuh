@@ -35,6 +35,9 @@ struct SearchArgs {
   uint32_t* gtab;
   uint32_t* ovf_list;
   uint32_t* ovf_count;
+  // if set, warps claim work items dynamically (atomicAdd) instead of the static
+  // stride: queries differ in cost, so this evens out the grid's tail
+  uint32_t* work_ctr;
   // outputs (indexed by query id)
   int64_t* out_slots;
   double* out_dists;
