@@ -98,9 +98,17 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bruteforce(BfArgs a) {
       bool ok[G];
       uint32_t slot[G];
       float4 x[G][NC];
+      // the row loads do not wait for the attribute test (every row of the span
+      // is mapped; rows that fail it are dropped after the reduction)
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        uint32_t p = base + g;
+        const uint32_t p = base + g;
+        const uint32_t pc = p < p1 ? p : p0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          uint32_t col = (c * 32 + lane) * 4;
+          x[g][c] = col < a.dp ? ldg_nc_f4(a.X + (uint64_t)pc * a.dp + col) : make_float4(0, 0, 0, 0);
+        }
         ok[g] = false;
         slot[g] = kNoSlot;
         if (p < p1) {
@@ -108,20 +116,24 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bruteforce(BfArgs a) {
           slot[g] = at.slot;
           ok[g] = at.slot < a.n_live && at.s >= lo_f && at.s <= hi_f;
         }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          uint32_t col = (c * 32 + lane) * 4;
-          x[g][c] = (ok[g] && col < a.dp) ? ldg_nc_f4(a.X + (uint64_t)p * a.dp + col) : make_float4(0, 0, 0, 0);
-        }
       }
+      double part[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        if (!ok[g]) continue;  // uniform: same row for all lanes
         double acc = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) acc = sq4(x[g][c], q[c], acc);
-        acc = warp_sum(acc);
-        list_insert(ld, ls, k, acc, slot[g]);
+        part[g] = acc;
+      }
+      // one scatter-reduction for the G rows (same pairing tree as warp_sum:
+      // bit-identical), row g's sum on lane g << SH
+      const double sum = reduce_scatter<G>(part);
+      constexpr uint32_t SH = G == 8 ? 2 : (G == 4 ? 3 : (G == 2 ? 4 : 5));
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double dg = __shfl_sync(0xFFFFFFFFu, sum, (uint32_t)g << SH);
+        if (!ok[g]) continue;  // uniform: same row for all lanes
+        list_insert(ld, ls, k, dg, slot[g]);
       }
     }
   }
