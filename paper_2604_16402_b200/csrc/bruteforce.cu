@@ -33,6 +33,9 @@ struct BfArgs {
 };
 
 constexpr int kBfWarps = 8;
+#ifndef GRAB_BF_PF_STEPS
+#define GRAB_BF_PF_STEPS 2
+#endif
 
 // insert (d, s) into the sorted warp list (length k, +inf padded) if it beats the tail
 __device__ __forceinline__ void list_insert(double* ld, uint32_t* ls, uint32_t k, double d, uint32_t s) {
@@ -93,8 +96,17 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bruteforce(BfArgs a) {
     const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f), hi_b = bucket_of_f32(a.bound, a.m, hi_f);
     const uint32_t p0 = __ldg(a.bstart + lo_b), p1 = __ldg(a.bstart + hi_b) + __ldg(a.bcount + hi_b);
     constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : (NC <= 4 ? 2 : 1));
+    const uint32_t rowb = a.dp * 4;
     for (uint32_t base = p0 + wid * G; base < p1; base += kBfWarps * G) {
-      // G consecutive rows per warp step
+      // G consecutive rows per warp step; the warp's rows two steps ahead are
+      // one contiguous block: a single bulk L2 prefetch covers them
+      {
+        const uint32_t pf = base + GRAB_BF_PF_STEPS * kBfWarps * G;
+        if (lane == 0 && pf + G <= p1)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.X + (uint64_t)pf * a.dp),
+                       "r"(rowb * (uint32_t)G)
+                       : "memory");
+      }
       bool ok[G];
       uint32_t slot[G];
       float4 x[G][NC];
