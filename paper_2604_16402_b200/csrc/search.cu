@@ -636,20 +636,20 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
             }
           }
           __syncwarp();
-          // (2) drop SENTINEL / slot >= n, per-iteration unique, scalar pre-check
+          // (2) drop SENTINEL / slot >= n, scalar pre-check. Duplicates of an
+          // in-range id are admitted once by the visited set below; the
+          // per-iteration unique (np.unique, searcher.py:212) only feeds the
+          // `gathered` / `precheck_rejected` counters, so it runs beside the
+          // visited atomics (count_unique) instead of in front of them
           uint32_t cand_bits = 0;
-          if (!a.out_stats) {
-            // no SearchStats requested: the per-iteration unique only feeds the
-            // `gathered` / `precheck_rejected` counters -- duplicates of an
-            // in-range id are still admitted once, by the visited set below
 #pragma unroll
-            for (int t = 0; t < EPL; ++t) {
-              const float sv = __uint_as_float(at[t].x);
-              cand_bits |= (at[t].y < a.n_live && sv >= lo_f && sv <= hi_f) ? 1u << t : 0u;
-            }
-          } else {
-            // every first-probe CAS in flight before any is consumed; the table
-            // (load <= 1/4) is left all-zero again by undoing this iteration's inserts
+          for (int t = 0; t < EPL; ++t) {
+            const float sv = __uint_as_float(at[t].x);
+            cand_bits |= (at[t].y < a.n_live && sv >= lo_f && sv <= hi_f) ? 1u << t : 0u;
+          }
+          // every first-probe CAS in flight before any is consumed; the table
+          // (load <= 1/4) is left all-zero again by undoing this iteration's inserts
+          auto count_unique = [&]() {
             const uint32_t dmask = (1u << dlg) - 1;
             uint32_t hs[EPL], dc[EPL], act = 0, pend = 0;
 #pragma unroll
@@ -676,13 +676,11 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
               const bool uq = ((act >> t) & 1u) && dc[t] == 0u;
               if (uq) dd[hs[t]] = 0u;
               const float sv = __uint_as_float(at[t].x);
-              const bool inr = sv >= lo_f && sv <= hi_f;
               gath_l += uq;
-              rej_l += uq && !inr;
-              cand_bits |= (uq && inr) ? 1u << t : 0u;
+              rej_l += uq && !(sv >= lo_f && sv <= hi_f);
             }
-          }
-          __syncwarp();
+            __syncwarp();
+          };
           // (3) exact visited set: every first-probe atomic of the iteration in flight at once
           {
             uint32_t cur[EPL];
@@ -692,10 +690,12 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
                 const uint32_t o = v[t] - vis.base;
                 cur[t] = ((cand_bits >> t) & 1u) ? atomicOr(vtab + (o >> 5), 1u << (o & 31)) : 0u;
               }
+              if (a.out_stats) count_unique();  // overlaps the visited atomics' round trip
 #pragma unroll
               for (int t = 0; t < EPL; ++t)
                 if ((cur[t] >> ((v[t] - vis.base) & 31)) & 1u) cand_bits &= ~(1u << t);
             } else {
+              if (a.out_stats) count_unique();
               const uint32_t vmask = (1u << vlg) - 1;
               uint32_t h[EPL];
 #pragma unroll
