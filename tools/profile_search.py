@@ -24,6 +24,7 @@ ap.add_argument("--iters", type=int)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--points", default="")
+ap.add_argument("--sel", type=float, default=0.1)
 a = ap.parse_args()
 n, dim, cap, nq, itopk, width, iters = P[a.config]
 itopk = a.itopk or itopk
@@ -31,7 +32,7 @@ width = a.width or width
 iters = a.iters or iters
 X, S = ds.gen_lowrank(n, dim, seed=0)
 Q = ds.lowrank_queries(nq, dim, seed=1)
-lo, hi = ds.range_arrays(ds.generate_ranges(S, 0.1, nq, 0))
+lo, hi = ds.range_arrays(ds.generate_ranges(S, a.sel, nq, 0))
 gi, rep = g.build_index(X, S, g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap))
 points = [(itopk, width, iters)]
 if a.points:
