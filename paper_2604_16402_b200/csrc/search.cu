@@ -524,7 +524,9 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
 #ifndef GRAB_SEARCH_MINB
 #define GRAB_SEARCH_MINB 6
 #endif
-template <int NC, int EPL, bool FULL>
+// STATS: SearchStats requested (the per-iteration unique count is compiled in
+// only then: its code costs the stats-free instance ~2 % even when skipped)
+template <int NC, int EPL, bool FULL, bool STATS>
 __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARCH_MINB))
     k_search(SearchArgs a, SearchShape sh) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -690,12 +692,12 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
                 const uint32_t o = v[t] - vis.base;
                 cur[t] = ((cand_bits >> t) & 1u) ? atomicOr(vtab + (o >> 5), 1u << (o & 31)) : 0u;
               }
-              if (a.out_stats) count_unique();  // overlaps the visited atomics' round trip
+              if constexpr (STATS) count_unique();  // overlaps the visited atomics' round trip
 #pragma unroll
               for (int t = 0; t < EPL; ++t)
                 if ((cur[t] >> ((v[t] - vis.base) & 31)) & 1u) cand_bits &= ~(1u << t);
             } else {
-              if (a.out_stats) count_unique();
+              if constexpr (STATS) count_unique();
               const uint32_t vmask = (1u << vlg) - 1;
               uint32_t h[EPL];
 #pragma unroll
@@ -766,14 +768,16 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
       a.out_slots[(uint64_t)qi * a.k + i] = s;
       a.out_dists[(uint64_t)qi * a.k + i] = d;
     }
+    if constexpr (STATS) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      gath_l += __shfl_xor_sync(kFull, gath_l, o);
-      rej_l += __shfl_xor_sync(kFull, rej_l, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        gath_l += __shfl_xor_sync(kFull, gath_l, o);
+        rej_l += __shfl_xor_sync(kFull, rej_l, o);
+      }
     }
     if (lane == 0) {
       a.out_counts[qi] = cnt;
-      if (a.out_stats) {
+      if (STATS && a.out_stats) {
         grab_search_stats st;
         st.iterations = iterations;
         st.dist_evals = dist_evals;
@@ -862,16 +866,16 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   return s;
 }
 
-// Calls f(kernel) with the k_search instance for (nc, epl, full).
+// Calls f(kernel) with the k_search instance for (nc, epl, full, stats).
 template <typename F>
-static void with_kernel(uint32_t nc, uint32_t epl, bool full, F&& f) {
-#define GRAB_K(NC_, EPL_)                      \
-  if (nc == NC_ && epl == EPL_) {              \
-    if (full)                                  \
-      f(k_search<NC_, EPL_, true>);            \
-    else                                       \
-      f(k_search<NC_, EPL_, false>);           \
-    return;                                    \
+static void with_kernel(uint32_t nc, uint32_t epl, bool full, bool stats, F&& f) {
+#define GRAB_K(NC_, EPL_)                                         \
+  if (nc == NC_ && epl == EPL_) {                                 \
+    if (full)                                                     \
+      stats ? f(k_search<NC_, EPL_, true, true>) : f(k_search<NC_, EPL_, true, false>);   \
+    else                                                          \
+      stats ? f(k_search<NC_, EPL_, false, true>) : f(k_search<NC_, EPL_, false, false>); \
+    return;                                                       \
   }
   GRAB_K(1, 1) GRAB_K(1, 2) GRAB_K(1, 4) GRAB_K(2, 1) GRAB_K(2, 2) GRAB_K(2, 4)
   GRAB_K(4, 1) GRAB_K(4, 2) GRAB_K(4, 4) GRAB_K(8, 1) GRAB_K(8, 2) GRAB_K(8, 4)
@@ -900,8 +904,9 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   // cost tens of microseconds, so they run once per configuration and device
   int dev = 0;
   GRAB_CUDA(cudaGetDevice(&dev));
+  const bool stats = a.out_stats != nullptr;
   const uint64_t key = ((uint64_t)dev << 48) | ((uint64_t)nc << 40) | ((uint64_t)epl << 36) |
-                       ((uint64_t)full << 35) | smem;
+                       ((uint64_t)full << 35) | ((uint64_t)stats << 34) | smem;
   static std::mutex occ_mu;
   static std::map<uint64_t, int> occ;
   int per_sm = 0;
@@ -911,7 +916,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
     if (it != occ.end()) {
       per_sm = it->second;
     } else {
-      with_kernel(nc, epl, full, [&](auto kern) {
+      with_kernel(nc, epl, full, stats, [&](auto kern) {
         // the attribute is per kernel instance: always the device maximum, so a
         // later, smaller configuration never lowers it under a cached larger one
         GRAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -929,7 +934,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
   const uint64_t words = blocks * wpb * (1ull << sh.vlog2);
   tables.ensure(words * 4, st);
   a.gtab = (uint32_t*)tables.p;
-  with_kernel(nc, epl, full, [&](auto kern) {
+  with_kernel(nc, epl, full, stats, [&](auto kern) {
     kern<<<(uint32_t)blocks, 32 * wpb, smem, st>>>(a, sh);
     GRAB_CHECK_LAUNCH();
   });
