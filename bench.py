@@ -197,6 +197,176 @@ def cpu_search_qps(idx, Q, lo, hi, seeds, point, procs: int, steps: int, warmup:
     return len(Q) * steps / el, el, slots
 
 
+# ------------------------------------------------------------------ selectivity sweep
+SWEEP_SELS = (0.01, 0.02, 0.05, 0.2, 0.5)
+
+
+def _event_ms(fn, stream, reps: int) -> float:
+    """Median CUDA-event time (ms) of fn() on `stream` over `reps` runs."""
+    import torch
+    out = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return sorted(out)[len(out) // 2]
+
+
+def selectivity_sweep(g, ds, gi, S, Q, dev, dim, hbm, target, sels=SWEEP_SELS, steps=5):
+    """QPS @ R@10 >= target at every selectivity of BASELINE configs[1]'s sweep.
+
+    Per selectivity: fixed-width ranges (generate_ranges, seed 0), exact truth
+    from the GPU brute force, then the smallest itopk (multiple of 8, bisection;
+    recall grows with itopk) reaching the target at max_iterations 100 and 150,
+    width 4; the faster of the two is the operating point. Its QPS is the median
+    of `steps` event-timed launches with device-resident inputs; `frac` is the
+    kernel's algorithmic bytes (its own counters) / time / measured HBM peak."""
+    import torch
+    from paper_2604_16402_b200 import _lib
+    stream = torch.cuda.current_stream(dev)
+    nq = len(Q)
+    Qd = torch.from_numpy(Q).to(dev)
+    out = {}
+    for sel in sels:
+        lo, hi = ds.range_arrays(ds.generate_ranges(S, sel, nq, 0))
+        truth, _, tc = g.brute_force_arrays(gi, Q, lo, hi, 10)
+        lod, hid = torch.from_numpy(lo).to(dev), torch.from_numpy(hi).to(dev)
+
+        def recall_of(itopk, iters):
+            sp = g.SearchParams(k=10, itopk=itopk, search_width=4, max_iterations=iters)
+            r = g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False)
+            return ds.batch_recall(r.slots.cpu().numpy(), r.counts.cpu().numpy(), truth, tc, 10)
+
+        best = None
+        for iters in (100, 150):
+            lo_t, hi_t = 4, 256  # itopk / 8 in (lo_t, hi_t]: recall(8 * hi_t) >= target
+            if recall_of(8 * hi_t, iters) < target:
+                continue
+            while hi_t - lo_t > 1:
+                mid = (lo_t + hi_t) // 2
+                if recall_of(8 * mid, iters) >= target:
+                    hi_t = mid
+                else:
+                    lo_t = mid
+            sp = g.SearchParams(k=10, itopk=8 * hi_t, search_width=4, max_iterations=iters)
+            ms = _event_ms(lambda: g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False), stream, steps)
+            if best is None or ms < best[0]:
+                best = (ms, sp)
+        if best is None:
+            out[str(sel)] = {"reached": False}
+            continue
+        ms, sp = best
+        r = g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0)
+        rec = ds.batch_recall(r.slots.cpu().numpy(), r.counts.cpu().numpy(), truth, tc, 10)
+        stats = np.frombuffer(r.stats.cpu().numpy().astype(np.uint32).tobytes(), dtype=_lib.STATS_DTYPE)
+        # the stats instance is the one whose bytes are counted; time it too
+        ms_stats = _event_ms(lambda: g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0), stream, steps)
+        b = algorithmic_bytes(stats, (dim + 3) // 4 * 4, 32, 10)
+        out[str(sel)] = {"qps": round(nq / (ms / 1e3), 1), "recall_at_10": round(rec, 4), "itopk": sp.itopk,
+                         "search_width": 4, "max_iterations": sp.max_iterations,
+                         "frac": round(b / (ms_stats / 1e3) / 1e9 / hbm, 4),
+                         "bytes_per_query": round(b / nq, 1)}
+        print(f"[bench] sel {sel}: {out[str(sel)]}", file=sys.stderr, flush=True)
+    return out
+
+
+# ------------------------------------------------------------------ cfg1 side by side
+def cfg1_side_by_side(g, ds, dev, local, hbm, target, cpu: bool):
+    """BASELINE configs[0] ("CPU reference runs"): 100K x 128 low-rank-16, cap 6 250
+    (m = 16), 1K range queries at 10 %, k = 10 -- the same three operations on the
+    GPU and on the host in one process:
+
+    * build: device build_index (median of 3) vs the reference's build restated
+      (oracle/construct.build, pinned byte-identical to bucketann's containers;
+      numpy + OpenBLAS on every host core, single process like build_index);
+    * search: QPS @ R@10 >= target on each side's OWN graph, same operating-point
+      rule (smallest itopk on the GPU graph, width 4, 50 / 100 iterations); the
+      CPU runs the numpy port of searcher.py over a fork pool of every core;
+    * insert: one 500-vector append-only batch into each side's graph (the
+      reference's insert_batch restated, single process, vs the device pipeline).
+    """
+    import torch
+    stream = torch.cuda.current_stream(dev)
+    n, dim, cap, nq, sel = 100_000, 128, 6_250, 1000, 0.10
+    X, S = ds.gen_lowrank(n, dim, seed=0)
+    Q = ds.lowrank_queries(nq, dim, seed=1)
+    lo, hi = ds.range_arrays(ds.generate_ranges(S, sel, nq, 0))
+    Xi, Si = ds.gen_lowrank(500, dim, seed=2, w_seed=0)
+    params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=cap)
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gi, brep = g.build_index(X, S, params, device=local)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    truth, _, tc = g.brute_force_arrays(gi, Q, lo, hi, 10)
+    Qd, lod, hid = (torch.from_numpy(a).to(dev) for a in (Q, lo, hi))
+    point = None
+    for iters in (50, 100):
+        for itopk in range(16, 513, 8):
+            sp = g.SearchParams(k=10, itopk=itopk, search_width=4, max_iterations=iters)
+            r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0, stats=False)
+            rec = ds.batch_recall(r.slots, r.counts, truth, tc, 10)
+            if rec >= target:
+                ms = _event_ms(lambda: g.search_arrays(gi, Qd, lod, hid, sp, seed_base=0, stats=False), stream, 21)
+                if point is None or ms < point[0]:
+                    point = (ms, sp, rec)
+                break
+    ms, sp, rec = point
+    torch.cuda.synchronize()
+    gi_ins = g.build_index(X, S, params, device=local)[0]
+    t0 = time.perf_counter()
+    g.insert_batch(gi_ins, Xi, Si)
+    torch.cuda.synchronize()
+    gpu_ins = len(Xi) / (time.perf_counter() - t0)
+    out = {"workload": f"cfg1: {n}x{dim} fp32 low-rank-16, bucket_capacity {cap} (m={brep.m}), {nq} range queries "
+                       f"at 10% selectivity, k=10; insert = one {len(Xi)}-vector batch",
+           "gpu": {"build_s": round(sorted(times)[1], 4), "qps": round(nq / (ms / 1e3), 1),
+                   "recall_at_10": round(rec, 4), "itopk": sp.itopk, "search_width": 4,
+                   "max_iterations": sp.max_iterations, "insert_vectors_per_s": round(gpu_ins, 1),
+                   "global_pass": brep.global_pass}}
+    if not cpu:
+        return out
+    from oracle import beam, construct, index_state as ist, ingest
+    procs = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    cidx, _, _ = construct.build(X, S, ist.BuildCfg(k_max=32, k_local=16, bucket_capacity=cap))
+    cpu_build = time.perf_counter() - t0
+    # the CPU graph's own operating point on the CPU graph: judged with the exact truth
+    gcpu = g.load_index(ist.container_bytes(cidx), params, device=local)
+    seeds = [beam.derive_seed(0, i) for i in range(nq)]
+    cpoint = None
+    for iters in (50, 100):
+        for itopk in range(16, 513, 8):
+            csp = g.SearchParams(k=10, itopk=itopk, search_width=4, max_iterations=iters)
+            r = g.search_arrays(gcpu, Q, lo, hi, csp, seed_base=0, stats=False)
+            if ds.batch_recall(r.slots, r.counts, truth, tc, 10) >= target:
+                if cpoint is None or itopk < cpoint.itopk:
+                    cpoint = csp
+                break
+    cq, _, cslots = cpu_search_qps(cidx, Q, lo, hi, seeds, (cpoint.itopk, 4, cpoint.max_iterations), procs, 1)
+    crec = ds.batch_recall(np.array([cslots[i] + [-1] * (10 - len(cslots[i])) for i in range(nq)]),
+                           np.array([len(cslots[i]) for i in range(nq)]), truth, tc, 10)
+    t0 = time.perf_counter()
+    ingest.insert(cidx, Xi, Si)  # N_cap = 2n (build_index headroom): room for the batch
+    cpu_ins = len(Xi) / (time.perf_counter() - t0)
+    out["cpu"] = {"kind": "port", "cores": procs, "build_s": round(cpu_build, 2), "qps": round(cq, 1),
+                  "recall_at_10": round(crec, 4), "itopk": cpoint.itopk, "max_iterations": cpoint.max_iterations,
+                  "insert_vectors_per_s": round(cpu_ins, 2),
+                  "what": "the reference's algorithm restated in numpy (oracle/, pinned to bucketann goldens): "
+                          "build single process (OpenBLAS GEMMs on all cores), search over a fork pool of "
+                          f"{procs}, insert single process"}
+    out["gpu_over_cpu"] = {"build": round(cpu_build / out["gpu"]["build_s"], 1),
+                           "search_qps": round(out["gpu"]["qps"] / cq, 1),
+                           "insert": round(gpu_ins / cpu_ins, 1)}
+    return out
+
+
 # ------------------------------------------------------------------ cfg4 / cfg5
 def _timed(fn, stream):
     """CUDA-event time (ms) of fn() on `stream`, synchronized on both sides."""
@@ -385,6 +555,55 @@ def run_sharded(args, cfg, rank, world, local, dist):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ reference arm
+def run_reference_arm(args, cfg, local):
+    """--impl reference: the reference's algorithm on the host cores (the numpy
+    port in oracle/, pinned to bucketann's goldens; the reference is pure Python,
+    nothing to compile), same config / metric / unit as the GPU arm.
+
+    The graph it searches is the configuration's index, produced by a child
+    process (this script with --export-graph: build + operating point on the
+    GPU, written as a GRAB v1 container); this process reads the container with
+    the oracle's reader and never loads libgrab.so. The reference's own CPU build
+    at 1M rows takes ~45 min; configs[0]'s CPU build is timed in the
+    GPU arm's line ("cfg1")."""
+    import tempfile
+    from oracle import beam, index_state as ist
+    with tempfile.TemporaryDirectory() as td:
+        base = os.path.join(td, "fixture")
+        env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK=str(local))
+        for key in ("MASTER_ADDR", "MASTER_PORT", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK", "TORCHELASTIC_RUN_ID"):
+            env.pop(key, None)
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "grab", "--config", args.config,
+               "--export-graph", base, "--warmup", "3", "--steps", "3"]
+        for key in ("n", "dim", "cap", "nq", "sel"):
+            if getattr(args, key) is not None:
+                cmd += [f"--{'rows' if key == 'n' else key}", str(getattr(args, key))]
+        subprocess.run(cmd, check=True, env=env, stdout=subprocess.DEVNULL)
+        with open(base + ".json") as f:
+            meta = json.load(f)
+        fx = np.load(base + ".npz")
+        with open(base + ".grab", "rb") as f:
+            idx = ist.index_from_container(f.read())
+    itopk, width, iters = meta["point"]
+    Q, lo, hi = fx["Q"], fx["lo"], fx["hi"]
+    m = len(Q)
+    procs = os.cpu_count() or 1
+    seeds = [beam.derive_seed(int(fx["seed_base"]), i) for i in range(m)]
+    steps = args.steps
+    qps, el, _ = cpu_search_qps(idx, Q, lo, hi, seeds, (itopk, width, iters), procs, steps, args.warmup)
+    line = {"impl": "reference", "metric": "range-filtered QPS @ recall@10=0.95", "value": round(qps, 2),
+            "unit": "queries/s", "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": el / steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": meta["config"],
+            "cpu_baseline": {"value": round(qps, 2), "unit": "queries/s", "cores": procs, "kind": "port",
+                             "sample": f"{m} of the {cfg['nq']} queries per step x {steps} steps of the numpy port "
+                                       f"of searcher.py (oracle/beam.py), fork pool of {procs}, on the "
+                                       "configuration's graph read from a GRAB v1 container"},
+            "e2e": {"value": round(qps, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -401,6 +620,9 @@ def main():
     ap.add_argument("--target", type=float, default=0.95)
     ap.add_argument("--cpu-sample", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the 1-50 %% selectivity sweep")
+    ap.add_argument("--no-cfg1", action="store_true", help="skip the configs[0] GPU-vs-CPU side-by-side leg")
+    ap.add_argument("--export-graph", help=argparse.SUPPRESS)  # reference-arm fixture (internal)
     ap.add_argument("--insert-batch", type=int, default=100_000)
     ap.add_argument("--inserts", type=int, help="cfg4: rows inserted after the build")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
@@ -418,7 +640,9 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    if args.impl == "reference" and rank != 0:
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args, cfg, local)
         return
     import torch
     # GRAB_BENCH_SHARED_GPU=1 (control-flow testing only): more ranks than GPUs,
@@ -517,26 +741,15 @@ def main():
               "build_timing": "median of 3 build_index calls (host arrays in, upload included; host wall "
                               "clock) after one untimed 120K-row warm-up build"}
 
-    if args.impl == "reference":
+    if args.export_graph:
+        # fixture for the reference arm (a separate process that never loads libgrab):
+        # the graph as a GRAB v1 container, the operating point, the query sample
+        g.save_index(gi, args.export_graph + ".grab")
         procs = os.cpu_count() or 1
-        idx = oracle_index_from(gi)
-        # each step = one pass over a bounded sample (8 queries per host core)
         m = min(8 * procs, nq)
-        seeds = [int(np.random.SeedSequence([seed_base, i]).generate_state(1, np.uint64)[0]) for i in range(m)]
-        steps = args.steps
-        qps, el, _ = cpu_search_qps(idx, Q[:m], lo[:m], hi[:m], seeds, (itopk, width, iters), procs, steps,
-                                    args.warmup)
-        line = {"impl": "reference", "metric": "range-filtered QPS @ recall@10=0.95", "value": round(qps, 2),
-                "unit": "queries/s", "n_gpus": 1, "steps": steps, "warmup": args.warmup,
-                "ms_per_step": el / steps * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": config,
-                "cpu_baseline": {"value": round(qps, 2), "unit": "queries/s", "cores": procs, "kind": "port",
-                                 "sample": f"{m} of the {nq} queries per step x {steps} steps of the numpy port of "
-                                           f"searcher.py (oracle/beam.py) "
-                                           f"on the same graph (built on the GPU, exported to slot layout), fork pool of {procs}"},
-                "e2e": {"value": round(qps, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        np.savez(args.export_graph + ".npz", Q=Q[:m], lo=lo[:m], hi=hi[:m], seed_base=seed_base)
+        with open(args.export_graph + ".json", "w") as f:
+            json.dump({"config": config, "point": [itopk, width, iters]}, f)
         return
 
     # ---- timed region: device-resident inputs, one search launch per step
@@ -634,6 +847,33 @@ def main():
     h2d = Q.nbytes + lo.nbytes + hi.nbytes
     d2h = rh.slots.nbytes + rh.dists.nbytes + rh.counts.nbytes + rh.stats.nbytes
 
+    # ---- QPS @ R95 across the selectivity sweep of configs[1] (before the insert mutates the graph)
+    sel_sweep = None
+    if not args.no_sweep and world == 1:
+        sel_sweep = selectivity_sweep(g, ds, gi, S, Q, dev, dim, hbm, args.target)
+        sel_sweep[str(sel)] = {"qps": round(qps, 1), "recall_at_10": round(recall, 4), "itopk": itopk,
+                               "search_width": width, "max_iterations": iters,
+                               "frac": round(achieved / hbm, 4), "bytes_per_query": round(bytes_q / nq, 1),
+                               "headline": True}
+        sel_sweep = dict(sorted(sel_sweep.items(), key=lambda kv: float(kv[0])))
+
+    # ---- e2e through the reference-shaped drop-in call: search_batch(index, Q, params)
+    # returns one SearchResult per query (shared range, searcher.py:236-248); the
+    # timed region includes reading every result's slots
+    sb_params = g.SearchParams(k=10, itopk=itopk, search_width=width, max_iterations=iters,
+                               range=g.RangePredicate(float(lo[0]), float(hi[0])))
+    g.search_batch(gi, Qh, sb_params)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    for _ in range(e2e_steps):
+        rs = g.search_batch(gi, Qh, sb_params)
+        touched = sum(len(r.slots) for r in rs)
+    sb_s = (time.perf_counter() - t3) / e2e_steps
+    e2e_search_batch = {"value": round(world * nq / sb_s, 1), "unit": "queries/s",
+                        "call": "search_batch(index, Q[pinned], params) -> list of SearchResult, every "
+                                "result's slots read", "range": "one shared range per batch (the reference's "
+                                "search_batch contract)", "results_read": int(touched)}
+
     # the CPU baseline searches the same graph: export it before the insert mutates it
     cpu_idx = oracle_index_from(gi) if (rank == 0 and world == 1 and not args.no_cpu) else None
 
@@ -689,7 +929,8 @@ def main():
                          "algorithmic_bytes_per_launch": round(bytes_q), "bytes_per_query": round(bytes_q / nq, 1),
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/search_traffic.json)"},
             # per step: the search grid + the (normally empty) overflow-retry grid
-            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "sweep": sweep}
+            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "e2e_search_batch": e2e_search_batch,
+            "selectivity_sweep": sel_sweep, "sweep": sweep}
     if remeasured:
         line["remeasured"] = remeasured
     if cpu_idx is not None:
@@ -715,6 +956,10 @@ def main():
                                 "result_agreement": float(agree),
                                 "insert_vectors_per_s": round(cpu_ins, 2),
                                 "insert_sample": f"{ci} vectors into the same {n}-row graph, single process"}
+    if rank == 0 and world == 1 and args.config == "cfg2" and not args.no_cfg1:
+        # configs[0] with the CPU reference beside it (after every GPU measurement above)
+        del gi
+        line["cfg1"] = cfg1_side_by_side(g, ds, dev, local, hbm, args.target, cpu=not args.no_cpu)
     if rank == 0:
         print(json.dumps(line))
     if dist:

@@ -138,6 +138,24 @@ GRAB_API int grab_build_ex(grab_index* h, const float* vectors, const float* sca
                            int strategy, uint32_t k_g, uint32_t refine_rounds, uint32_t mem,
                            grab_build_report* report, const grab_build_debug* debug);
 
+/* ---- the build phases on an imported state (grab_import: rows, scalars,
+ * bucket maps; SENTINEL or draft adjacency), for the reference's phase-level
+ * API. flags: 0 = pass 1 + pass 2 + fuse + repair (build_index minus the
+ * partition), GRAB_GRAPH_LOCAL_ONLY = pass 1 (build_local_phase,
+ * builder.py:237-261), GRAB_GRAPH_GLOBAL_ONLY = pass 2 (build_global_graph,
+ * builder.py:364-393: exact kNN iff count <= exact_limit, else random init +
+ * refine_rounds NN-descent rounds). Intermediate rows via `debug`. */
+#define GRAB_GRAPH_LOCAL_ONLY 1
+#define GRAB_GRAPH_GLOBAL_ONLY 2
+GRAB_API int grab_build_graph(grab_index* h, uint32_t k_g, uint32_t refine_rounds, uint64_t exact_limit,
+                              uint32_t flags, grab_build_report* report, const grab_build_debug* debug);
+/* fuse_remote_edges (builder.py:396-452): the index adjacency holds the draft
+ * rows (imported); necessary [count] and global_rows [count x k_g] are host,
+ * slot space. Read the fused rows back with grab_read(GRAB_ARR_ADJ). */
+GRAB_API int grab_fuse(grab_index* h, const uint32_t* necessary, const uint32_t* global_rows, uint32_t k_g);
+/* reinforce_reachability (builder.py:455-500) on the live rows; *added = links added */
+GRAB_API int grab_reinforce(grab_index* h, uint64_t* added);
+
 /* ---- insert_batch (updater.py:154-263) ---- */
 GRAB_API int grab_insert(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids,
                 uint64_t b, uint32_t search_itopk, uint32_t mem, grab_insert_report* report);

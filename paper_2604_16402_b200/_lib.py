@@ -20,6 +20,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 SENTINEL = 0xFFFFFFFF
 LIVE_ALL = 0xFFFFFFFFFFFFFFFF
 ARR_X, ARR_SCALARS, ARR_ADJ, ARR_I2B, ARR_BOUNDARIES, ARR_B2I_OFFSETS, ARR_B2I_FLAT = range(7)
+GRAPH_LOCAL_ONLY, GRAPH_GLOBAL_ONLY = 1, 2
 
 
 class GrabDeviceError(RuntimeError):
@@ -80,6 +81,9 @@ _SIGS = {
     "grab_sync": (C.c_int, [P]),
     "grab_build": (C.c_int, [P, P, P, u64, C.c_int, u32, u32, u32, C.POINTER(BuildReportC)]),
     "grab_build_ex": (C.c_int, [P, P, P, u64, C.c_int, u32, u32, u32, C.POINTER(BuildReportC), P]),
+    "grab_build_graph": (C.c_int, [P, u32, u32, u64, u32, C.POINTER(BuildReportC), P]),
+    "grab_fuse": (C.c_int, [P, P, P, u32]),
+    "grab_reinforce": (C.c_int, [P, C.POINTER(u64)]),
     "grab_insert": (C.c_int, [P, P, P, P, u64, u32, u32, C.POINTER(InsertReportC)]),
     "grab_last_rewired": (C.c_int, [P, P, u64, C.POINTER(u64)]),
     "grab_append": (C.c_int, [P, P, P, P, u64, u32, C.POINTER(u64), C.POINTER(u64)]),

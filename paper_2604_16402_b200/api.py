@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -62,19 +63,64 @@ class BatchResult:
     stats: np.ndarray | None
     elapsed_s: float
 
-    def to_results(self, k: int) -> list[SearchResult]:
-        out = []
-        per = self.elapsed_s / max(len(self.counts), 1)
-        for i in range(len(self.counts)):
-            c = int(self.counts[i])
-            st = SearchStats(**{f: int(self.stats[i][f]) for f in L.STAT_FIELDS}, elapsed_s=per) \
-                if self.stats is not None else SearchStats(elapsed_s=per)
-            out.append(SearchResult(self.slots[i, :c].copy(), self.dists[i, :c].copy(), 0 < c < k, st))
-        return out
+    def to_results(self, k: int) -> "ResultList":
+        return ResultList(self, k)
+
+
+class ResultList(Sequence):
+    """search_batch's list of SearchResult (searcher.py:236-248), materialised per
+    item on access: the batch arrays stay as they came back from the kernel and
+    each SearchResult's slots / sq_dists are views of its row, so returning a
+    10K-query batch costs nothing per query until a caller reads it."""
+
+    def __init__(self, batch: BatchResult, k: int):
+        self._b = batch
+        self._k = k
+        self._counts = np.asarray(batch.counts).tolist()
+        self._stats = None if batch.stats is None else np.asarray(batch.stats).tolist()
+        self._per = batch.elapsed_s / max(len(self._counts), 1)
+
+    def __len__(self) -> int:
+        return len(self._counts)
+
+    def _item(self, i: int) -> SearchResult:
+        c = self._counts[i]
+        st = SearchStats(*self._stats[i], elapsed_s=self._per) if self._stats is not None else \
+            SearchStats(elapsed_s=self._per)
+        return SearchResult(self._b.slots[i, :c], self._b.dists[i, :c], 0 < c < self._k, st)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._item(j) for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self._item(i)
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self._item(i)
 
 
 def _is_dev(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _check_dev(t, name: str, dtype: str, ndim: int, index: GraphIndex):
+    """Device-path argument checks (the host path gets the same from numpy
+    conversion): libgrab reads raw pointers, so dtype / rank / device must match."""
+    import torch
+    want = getattr(torch, dtype)
+    if not (hasattr(t, "is_cuda") and t.is_cuda):
+        raise ValueError(f"{name} must be a CUDA tensor when the other inputs are")
+    if t.dtype != want:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != ndim:
+        raise DimensionMismatchError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
+    if t.device.index != index.device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the index on cuda:{index.device}")
+    return t.contiguous()
 
 
 def _is_pinned(a) -> bool:
@@ -112,7 +158,7 @@ def search_arrays(index: GraphIndex, queries, lower, upper, params: SearchParams
     dev = _is_dev(queries)
     if dev:
         import torch
-        Q = queries.contiguous()
+        Q = _check_dev(queries, "queries", "float32", 2, index)
         nq, d = Q.shape
         lo = torch.as_tensor(lower, dtype=torch.float64, device=Q.device).reshape(-1).contiguous()
         hi = torch.as_tensor(upper, dtype=torch.float64, device=Q.device).reshape(-1).contiguous()
@@ -163,12 +209,16 @@ def search(index: GraphIndex, query, params: SearchParams, *, live_count=None) -
     q = np.asarray(query, dtype=np.float32).reshape(1, -1)
     r = search_arrays(index, q, params.range.lower, params.range.upper, params,
                       seeds=np.array([params.rng_seed], dtype=np.uint64), live_count=live_count)
-    return r.to_results(params.k)[0]
+    res = r.to_results(params.k)[0]
+    return SearchResult(res.slots.copy(), res.sq_dists.copy(), res.truncated, res.stats)
 
 
-def search_batch(index: GraphIndex, queries, params: SearchParams, *, live_count=None) -> list[SearchResult]:
-    """searcher.py:236-248: shared range, seeds derive_query_seed(params.rng_seed, i)."""
-    Q = np.asarray(queries, dtype=np.float32)
+def search_batch(index: GraphIndex, queries, params: SearchParams, *, live_count=None) -> Sequence:
+    """searcher.py:236-248: shared range, seeds derive_query_seed(params.rng_seed, i).
+
+    Returns a sequence of SearchResult (``ResultList``, built per item on access).
+    A page-locked torch CPU tensor of queries takes the zero-copy path."""
+    Q = queries if _is_pinned(queries) else np.asarray(queries, dtype=np.float32)
     if len(Q) == 0:
         return []
     r = search_arrays(index, Q, params.range.lower, params.range.upper, params, live_count=live_count)
@@ -347,8 +397,16 @@ def build_index(vectors, scalars, params: BuildParams, *, capacity: int | None =
         import torch
         V = vectors.contiguous()
         S = scalars.contiguous()
-        torch.cuda.current_stream(V.device).synchronize()  # the library works on its own stream
+        if V.dtype != torch.float32 or V.dim() != 2:
+            raise DimensionMismatchError(f"vectors must be a 2-D float32 tensor, got {V.dtype} {tuple(V.shape)}")
+        if S.dtype != torch.float32 or S.dim() != 1 or S.device != V.device:
+            raise ValueError("scalars must be a 1-D float32 tensor on the vectors' device")
         n, dim = V.shape
+        if len(S) != n:
+            raise ValueError(f"{n} vectors but {len(S)} scalars")
+        if not bool(torch.isfinite(S).all()):
+            raise ValueError("scalars must be finite")
+        torch.cuda.current_stream(V.device).synchronize()  # the library works on its own stream
         mem = L.MEM_DEVICE
     else:
         V = np.ascontiguousarray(vectors, dtype=np.float32)
@@ -422,8 +480,10 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
     dev = _is_dev(vectors)
     if dev:
         import torch
-        V = vectors.contiguous()
-        S = scalars.contiguous()
+        V = _check_dev(vectors, "vectors", "float32", 2, index)
+        S = _check_dev(scalars, "scalars", "float32", 1, index)
+        if not bool(torch.isfinite(S).all()):
+            raise ValueError("scalars must be finite")
         torch.cuda.current_stream(V.device).synchronize()  # the library works on its own stream
         b = V.shape[0]
         mem = L.MEM_DEVICE
@@ -450,10 +510,10 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
                               C.byref(rep)))
     index._touch()
     n0 = index.count - b
+    head = int(rep.bulk_built)  # an empty index bulk-builds its head with ids arange(head), like the reference
+    index._ids[n0:n0 + b] = np.arange(n0, n0 + b)
     if Ih is not None:
-        index._ids[n0:n0 + b] = Ih
-    else:
-        index._ids[n0:n0 + b] = np.arange(n0, n0 + b)
+        index._ids[n0 + head:n0 + b] = Ih[head:]
     rw = np.empty(int(rep.n_rewired), dtype=np.uint32)
     nout = C.c_uint64()
     if len(rw):

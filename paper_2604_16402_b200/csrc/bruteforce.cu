@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(kBfWarps * 32) k_bruteforce(BfArgs a) {
     uint32_t col = (c * 32 + lane) * 4;
     q[c] = col < a.dp ? *reinterpret_cast<const float4*>(a.Q + qi * a.dp + col) : make_float4(0, 0, 0, 0);
   }
-  if (a.m > 0 && a.n_live > 0) {
+  // !(lo <= hi) (inverted or NaN bounds on the device path): empty result, never a
+  // wrapped bucket interval
+  if (a.m > 0 && a.n_live > 0 && lo_f <= hi_f) {
     const uint32_t lo_b = bucket_of_f32(a.bound, a.m, lo_f), hi_b = bucket_of_f32(a.bound, a.m, hi_f);
     const uint32_t p0 = __ldg(a.bstart + lo_b), p1 = __ldg(a.bstart + hi_b) + __ldg(a.bcount + hi_b);
     constexpr int G = NC == 1 ? 8 : (NC == 2 ? 4 : (NC <= 4 ? 2 : 1));

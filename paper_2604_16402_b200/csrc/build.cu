@@ -503,6 +503,11 @@ static void capture_rows(const DevIndex& ix, const uint32_t* src, uint32_t K, ui
   cudaFreeAsync(tmp, st);
 }
 
+__global__ void k_scatter_u32(const uint32_t* src, const uint32_t* s2p, uint64_t n, uint32_t* out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[s2p[i]] = src[i];
+}
+
 __global__ void k_gather_u32(const uint32_t* src, const uint32_t* s2p, uint64_t n, uint32_t* out) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = src[s2p[i]];
@@ -583,8 +588,9 @@ void descent_device(const DevIndex& ix, uint64_t n, uint32_t k, uint32_t rounds,
                     double* gd, cudaStream_t st);  // descent.cu
 
 void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_rounds, grab_build_report* rep,
-                        const grab_build_debug* dbg, cudaStream_t st) {
+                        const grab_build_debug* dbg, cudaStream_t st, uint32_t flags) {
   const uint32_t K = ix.params.k_max;
+  const bool local_pass = !(flags & kGraphGlobalOnly), rest = !(flags & kGraphLocalOnly);
   Scratch S(st);
   uint32_t* rows = S.alloc<uint32_t>(n);  // phys rows in slot order
   k_live_rows<<<(unsigned)div_up(n, 256), 256, 0, st>>>(ix.slot2phys, n, rows);
@@ -597,6 +603,7 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
 
   double t0 = now_s();
   // ---- pass 1: per-bucket kNN over slabs
+  if (local_pass) {
   uint32_t* fwd = S.alloc<uint32_t>(ix.phys_cap * (uint64_t)K);
   double* fd = S.alloc<double>(ix.phys_cap * (uint64_t)K);
   {
@@ -658,7 +665,13 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
       cudaFreeAsync(tmp, st);
     }
   }
+  }  // local_pass
   double t1 = now_s();
+  if (!rest) {
+    rep->phase1_seconds = t1 - t0;
+    rep->total_seconds = t1 - t0;
+    return;
+  }
 
   // ---- pass 2: global kNN over all live rows, then reverse merge
   uint32_t* G = S.alloc<uint32_t>(ix.phys_cap * (uint64_t)k_g);
@@ -712,6 +725,11 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
   GRAB_CUDA(cudaStreamSynchronize(st));
   if (dbg) capture_rows(ix, G, k_g, n, dbg->global_rows, st);
   double t2 = now_s();
+  if (!local_pass) {
+    rep->phase2_seconds = t2 - t1;
+    rep->total_seconds = t2 - t0;
+    return;
+  }
 
   // ---- fuse + repair
   {
@@ -739,6 +757,54 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
   rep->phase2_seconds = t2 - t1;
   rep->fuse_seconds = t3 - t2;
   rep->total_seconds = t3 - t0;
+}
+
+// fuse_remote_edges (builder.py:396-452) over explicit inputs: the index's
+// adjacency holds the draft rows (imported), `nec` / `G` are slot-space host
+// arrays (necessary counts [n], global rows [n x k_g]).
+__global__ void k_rows_slot_to_phys(const uint32_t* src, uint64_t n, uint32_t k, const uint32_t* s2p, uint32_t* dst) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n * k) return;
+  const uint32_t v = src[i];
+  dst[(uint64_t)s2p[i / k] * k + i % k] = (v == kSentinel || v >= n) ? kSentinel : s2p[v];
+}
+
+void fuse_device(DevIndex& ix, uint64_t n, const uint32_t* nec_host, const uint32_t* G_host, uint32_t k_g) {
+  cudaStream_t st = ix.stream;
+  Scratch S(st);
+  const uint32_t K = ix.params.k_max;
+  uint32_t* rows = S.alloc<uint32_t>(n);
+  k_live_rows<<<(unsigned)div_up(n, 256), 256, 0, st>>>(ix.slot2phys, n, rows);
+  GRAB_CHECK_LAUNCH();
+  uint32_t* nec_s = S.alloc<uint32_t>(n);
+  uint32_t* nec = S.alloc<uint32_t>(ix.phys_cap);
+  GRAB_CUDA(cudaMemsetAsync(nec, 0, ix.phys_cap * 4, st));
+  GRAB_CUDA(cudaMemcpyAsync(nec_s, nec_host, n * 4, cudaMemcpyHostToDevice, st));
+  k_scatter_u32<<<(unsigned)div_up(n, 256), 256, 0, st>>>(nec_s, ix.slot2phys, n, nec);
+  GRAB_CHECK_LAUNCH();
+  uint32_t* Gs = S.alloc<uint32_t>(n * (uint64_t)k_g);
+  uint32_t* G = S.alloc<uint32_t>(ix.phys_cap * (uint64_t)k_g);
+  GRAB_CUDA(cudaMemsetAsync(G, 0xFF, ix.phys_cap * (uint64_t)k_g * 4, st));
+  GRAB_CUDA(cudaMemcpyAsync(Gs, G_host, n * (uint64_t)k_g * 4, cudaMemcpyHostToDevice, st));
+  k_rows_slot_to_phys<<<(unsigned)div_up(n * k_g, 256), 256, 0, st>>>(Gs, n, k_g, ix.slot2phys, G);
+  GRAB_CHECK_LAUNCH();
+  const double span = (double)ix.h_bound.back() - (double)ix.h_bound.front();
+  const double window = ix.params.proximal_window * span;
+  const uint32_t quota = (uint32_t)std::nearbyint(ix.params.proximal_fraction * (double)(K - ix.params.k_local));
+  k_fuse<<<(unsigned)div_up(n, 256), 256, 0, st>>>(rows, n, G, k_g, ix.attr, ix.i2b, window, quota, K, nec, ix.adj);
+  GRAB_CHECK_LAUNCH();
+  GRAB_CUDA(cudaStreamSynchronize(st));
+}
+
+uint32_t reinforce_index_device(DevIndex& ix) {
+  cudaStream_t st = ix.stream;
+  const uint64_t n = ix.count;
+  if (!n) return 0;
+  Scratch S(st);
+  uint32_t* rows = S.alloc<uint32_t>(n);
+  k_live_rows<<<(unsigned)div_up(n, 256), 256, 0, st>>>(ix.slot2phys, n, rows);
+  GRAB_CHECK_LAUNCH();
+  return reinforce_device(ix, rows, n, st);
 }
 
 void build_index_device(DevIndex& ix, const float* vectors, const float* scalars, uint64_t n, int strategy,
@@ -789,7 +855,7 @@ void build_index_device(DevIndex& ix, const float* vectors, const float* scalars
   rep.n = n;
   rep.m = ix.m;
   if (ix.params.k_max > 64) throw Error(GRAB_ERR_VALUE, "k_max > 64 not supported");
-  build_graph_device(ix, n, k_g, refine_rounds, &rep, dbg, st);
+  build_graph_device(ix, n, k_g, refine_rounds, &rep, dbg, st, 0);
   ix.built = true;
   GRAB_CUDA(cudaStreamSynchronize(st));
   if (report) *report = rep;

@@ -4,7 +4,9 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <vector>
 
@@ -15,10 +17,45 @@
 
 using namespace grab;
 
+// Concurrency (layout.py:238-239): search / brute force / reads are
+// concurrent readers, build / import / insert / append exclusive topology
+// writers. Readers hold `rw` shared while they enqueue and record `done` on
+// their stream; a writer takes `rw` exclusive and makes its own stream wait for
+// every reader stream's last event before it rewires rows or relayouts (frees)
+// buffers, so no in-flight search ever reads a freed or half-rewired array.
+// Writers synchronize their stream before returning, so readers that start
+// afterwards see the last published count and the new pointers.
 struct grab_index {
   DevIndex ix;
-  std::mutex writer;  // build/insert are exclusive topology writers (SPEC concurrency model)
+  std::shared_mutex rw;
+  std::mutex readers_mu;
+  std::map<cudaStream_t, cudaEvent_t> readers;  // reader stream -> its last enqueued work
+  ~grab_index() {
+    for (auto& kv : readers) cudaEventDestroy(kv.second);
+  }
 };
+
+namespace {
+struct ReadLock {
+  grab_index* h;
+  std::shared_lock<std::shared_mutex> lk;
+  explicit ReadLock(const grab_index* hc) : h(const_cast<grab_index*>(hc)), lk(h->rw) {}
+  // after enqueueing on `st`: remember it so a later writer can wait for it
+  void done(cudaStream_t st) {
+    std::lock_guard<std::mutex> g(h->readers_mu);
+    cudaEvent_t& ev = h->readers[st];
+    if (!ev) GRAB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GRAB_CUDA(cudaEventRecord(ev, st));
+  }
+};
+struct WriteLock {
+  std::unique_lock<std::shared_mutex> lk;
+  explicit WriteLock(grab_index* h) : lk(h->rw) {
+    std::lock_guard<std::mutex> g(h->readers_mu);
+    for (auto& kv : h->readers) GRAB_CUDA(cudaStreamWaitEvent(h->ix.stream, kv.second, 0));
+  }
+};
+}  // namespace
 
 static thread_local std::string g_err;
 
@@ -213,6 +250,7 @@ extern "C" int grab_search(const grab_index* h, const float* queries, uint64_t n
                            grab_search_stats* out_stats, uint32_t mem, void* stream) {
   return guarded([&] {
     check_handle(h);
+    ReadLock rl(h);
     const DevIndex& ix = h->ix;
     set_device(ix);
     if (!p) throw Error(GRAB_ERR_VALUE, "null search params");
@@ -285,6 +323,7 @@ extern "C" int grab_search(const grab_index* h, const float* queries, uint64_t n
     copy_back(out_dists, bd, nq * p->k, smem, st);
     copy_back(out_counts, bc, nq, smem, st);
     copy_back(out_stats, bst, nq, smem, st);
+    rl.done(st);
     if (mem == GRAB_MEM_HOST) GRAB_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -295,6 +334,7 @@ extern "C" int grab_brute_force(const grab_index* h, const float* queries, uint6
                                 void* stream) {
   return guarded([&] {
     check_handle(h);
+    ReadLock rl(h);
     const DevIndex& ix = h->ix;
     set_device(ix);
     if (k < 1) throw Error(GRAB_ERR_VALUE, "k must be >= 1");
@@ -314,6 +354,7 @@ extern "C" int grab_brute_force(const grab_index* h, const float* queries, uint6
     copy_back(out_slots, bs, nq * k, mem, st);
     copy_back(out_dists, bd, nq * k, mem, st);
     copy_back(out_counts, bc, nq, mem, st);
+    rl.done(st);
     if (mem == GRAB_MEM_HOST) GRAB_CUDA(cudaStreamSynchronize(st));
     // `view` shares pointers with ix; release them without freeing
     view.X = nullptr;
@@ -324,6 +365,7 @@ extern "C" int grab_bucket_select(const grab_index* h, const double* lower, cons
                                   int32_t* out_lo, int32_t* out_hi, uint32_t mem, void* stream) {
   return guarded([&] {
     check_handle(h);
+    ReadLock rl(h);
     const DevIndex& ix = h->ix;
     set_device(ix);
     if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no bucket metadata (never built)");
@@ -337,6 +379,7 @@ extern "C" int grab_bucket_select(const grab_index* h, const double* lower, cons
     launch_bucket_select(ix, lo, hi, n, ol, oh, st);
     copy_back(out_lo, c, n, mem, st);
     copy_back(out_hi, d, n, mem, st);
+    rl.done(st);
     if (mem == GRAB_MEM_HOST) GRAB_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -345,6 +388,7 @@ extern "C" int grab_bucket_ids(const grab_index* h, const float* scalars, uint64
                                void* stream) {
   return guarded([&] {
     check_handle(h);
+    ReadLock rl(h);
     const DevIndex& ix = h->ix;
     set_device(ix);
     if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no bucket metadata (never built)");
@@ -355,6 +399,7 @@ extern "C" int grab_bucket_ids(const grab_index* h, const float* scalars, uint64
     int32_t* o = stage_out(out, n, mem, c, st);
     launch_bucket_ids(ix, s, n, o, st);
     copy_back(out, c, n, mem, st);
+    rl.done(st);
     if (mem == GRAB_MEM_HOST) GRAB_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -391,7 +436,7 @@ extern "C" int grab_import(grab_index* h, uint64_t n, const float* X, const floa
                            const uint32_t* b2i_flat, const uint64_t* b2i_offsets) {
   return guarded([&] {
     check_handle(h);
-    std::lock_guard<std::mutex> lk(h->writer);
+    WriteLock lk(h);
     DevIndex& ix = h->ix;
     set_device(ix);
     if (n > ix.n_cap) throw Error(GRAB_ERR_CAPACITY, "import exceeds capacity");
@@ -435,6 +480,7 @@ extern "C" int grab_import(grab_index* h, uint64_t n, const float* X, const floa
 extern "C" int grab_read(const grab_index* h, int what, uint64_t start, uint64_t count, void* out) {
   return guarded([&] {
     check_handle(h);
+    ReadLock rl(h);
     const DevIndex& ix = h->ix;
     set_device(ix);
     cudaStream_t st = ix.stream;
@@ -496,7 +542,7 @@ extern "C" int grab_build(grab_index* h, const float* vectors, const float* scal
                           uint32_t k_g, uint32_t refine_rounds, uint32_t mem, grab_build_report* report) {
   return guarded([&] {
     check_handle(h);
-    std::lock_guard<std::mutex> lk(h->writer);
+    WriteLock lk(h);
     DevIndex& ix = h->ix;
     set_device(ix);
     ix.adj_version++;
@@ -510,7 +556,7 @@ extern "C" int grab_build_ex(grab_index* h, const float* vectors, const float* s
                              const grab_build_debug* debug) {
   return guarded([&] {
     check_handle(h);
-    std::lock_guard<std::mutex> lk(h->writer);
+    WriteLock lk(h);
     DevIndex& ix = h->ix;
     set_device(ix);
     ix.adj_version++;
@@ -519,11 +565,73 @@ extern "C" int grab_build_ex(grab_index* h, const float* vectors, const float* s
   });
 }
 
+extern "C" int grab_build_graph(grab_index* h, uint32_t k_g, uint32_t refine_rounds, uint64_t exact_limit,
+                                uint32_t flags, grab_build_report* report, const grab_build_debug* debug) {
+  return guarded([&] {
+    check_handle(h);
+    WriteLock lk(h);
+    DevIndex& ix = h->ix;
+    set_device(ix);
+    if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no rows / bucket metadata (import first)");
+    if (ix.params.k_max > 64) throw Error(GRAB_ERR_VALUE, "k_max > 64 not supported");
+    if ((flags & 3) == 3) throw Error(GRAB_ERR_VALUE, "local-only and global-only are exclusive");
+    const uint64_t n = ix.count;
+    if (k_g == 0) k_g = ix.params.k_max;
+    grab_build_report rep{};
+    rep.n = n;
+    rep.m = ix.m;
+    // exact_limit (builder.py:364-393): exact kNN iff n <= exact_limit, else NN-descent
+    const uint32_t gp = ix.params.global_pass;
+    ix.params.global_pass = n <= exact_limit ? GRAB_GLOBAL_EXACT : GRAB_GLOBAL_DESCENT;
+    ix.adj_version++;
+    try {
+      if (n >= 2 || (flags & kGraphLocalOnly))
+        build_graph_device(ix, n, k_g, refine_rounds, &rep, debug, ix.stream, flags);
+    } catch (...) {
+      ix.params.global_pass = gp;
+      throw;
+    }
+    ix.params.global_pass = gp;
+    ix.adj_version++;
+    GRAB_CUDA(cudaStreamSynchronize(ix.stream));
+    if (report) *report = rep;
+  });
+}
+
+extern "C" int grab_fuse(grab_index* h, const uint32_t* necessary, const uint32_t* global_rows, uint32_t k_g) {
+  return guarded([&] {
+    check_handle(h);
+    WriteLock lk(h);
+    DevIndex& ix = h->ix;
+    set_device(ix);
+    if (!ix.built) throw Error(GRAB_ERR_STATE, "index has no rows / bucket metadata (import first)");
+    if (!necessary || !global_rows || k_g == 0) throw Error(GRAB_ERR_VALUE, "null fuse inputs");
+    for (uint64_t i = 0; i < ix.count; ++i)
+      if (necessary[i] > ix.params.k_max) throw Error(GRAB_ERR_VALUE, "necessary count > k_max");
+    ix.adj_version++;
+    if (ix.count) fuse_device(ix, ix.count, necessary, global_rows, k_g);
+    ix.adj_version++;
+  });
+}
+
+extern "C" int grab_reinforce(grab_index* h, uint64_t* added) {
+  return guarded([&] {
+    check_handle(h);
+    WriteLock lk(h);
+    DevIndex& ix = h->ix;
+    set_device(ix);
+    ix.adj_version++;
+    const uint32_t a = ix.built ? reinforce_index_device(ix) : 0;
+    ix.adj_version++;
+    if (added) *added = a;
+  });
+}
+
 extern "C" int grab_insert(grab_index* h, const float* vectors, const float* scalars, const int64_t* ids, uint64_t b,
                            uint32_t search_itopk, uint32_t mem, grab_insert_report* report) {
   return guarded([&] {
     check_handle(h);
-    std::lock_guard<std::mutex> lk(h->writer);
+    WriteLock lk(h);
     DevIndex& ix = h->ix;
     set_device(ix);
     ix.adj_version++;
@@ -536,7 +644,7 @@ extern "C" int grab_append(grab_index* h, const float* vectors, const float* sca
                            uint32_t mem, uint64_t* start, uint64_t* end) {
   return guarded([&] {
     check_handle(h);
-    std::lock_guard<std::mutex> lk(h->writer);
+    WriteLock lk(h);
     DevIndex& ix = h->ix;
     set_device(ix);
     ix.adj_version++;
@@ -649,6 +757,7 @@ uint64_t scc_count_device(const uint32_t* adj, uint32_t n, uint32_t K, cudaStrea
 extern "C" int grab_scc_count(const grab_index* h, uint64_t live_count, uint64_t* out) {
   return guarded([&] {
     check_handle(h);
+    ReadLock rl(h);
     const DevIndex& ix = h->ix;
     set_device(ix);
     const uint64_t n = live_of(ix, live_count);

@@ -753,9 +753,10 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
       return;
     }
     uint64_t head = std::min<uint64_t>(b, ix.params.bucket_capacity);
+    // the reference bulk-builds through build_index, which ignores ids: the head
+    // keeps ids = arange(head) (build_index_device sets them); only ids[head:]
+    // reach the appended tail (updater.py:175-189)
     build_index_device(ix, Vd, Sd, head, GRAB_STRATEGY_QUANTILE, ix.params.k_max, 3, GRAB_MEM_DEVICE, nullptr);
-    if (ids)
-      for (uint64_t i = 0; i < head; ++i) ix.ids[i] = ids[i];
     R.bulk_built = head;
     if (head == b) {
       R.wall_time_s = now_s() - t_begin;

@@ -565,7 +565,9 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
     uint32_t gath_l = 0, rej_l = 0;  // per-lane partial counts, summed at the end
     uint32_t L = 0;
     bool overflow = false;
-    if (a.n_live > 0 && a.m > 0) {
+    // !(lo <= hi) (inverted or NaN bounds reaching the kernel through the device
+    // path): an empty result, never a wrapped bucket interval (lo_b > hi_b)
+    if (a.n_live > 0 && a.m > 0 && lo_f <= hi_f) {
       QueryRegs<NC> qr;
       load_query<NC>(qr, a.qphys ? a.X + (uint64_t)a.qphys[qi] * a.dp : a.Q + (uint64_t)qi * a.dp, a.dp,
                      (float4*)(base + sh.o_q));
@@ -837,7 +839,7 @@ static uint32_t ceil_log2(uint64_t x) {
 }
 
 SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst,
-                       uint32_t dp) {
+                       uint32_t dp, uint64_t live_rows) {
   SearchShape s;
   const uint32_t nc = (dp + 127) / 128;
   s.qbytes = nc > 2 ? (nc <= 4 ? 4u : nc <= 8 ? 8u : 16u) * 512u : 0u;  // QueryRegs<NC>::kShared staging
@@ -851,7 +853,10 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
     // a 4K table overflowed every insert candidate search); a bitmap needs only nbits / 8 of it
     s.vlog2 = std::min<uint32_t>(15, std::max<uint32_t>(12, ceil_log2((uint64_t)itopk * 48)));
   } else {
-    const uint64_t bound = (uint64_t)want + (uint64_t)max_iter * fan + fan;
+    // every insert is a distinct in-range row, so the live row count bounds the
+    // table too (max_iterations is only a cap: 1e6 must not size a 5 GB table)
+    const uint64_t bound = std::min<uint64_t>((uint64_t)want + (uint64_t)max_iter * fan + fan,
+                                              (uint64_t)live_rows + fan);
     s.vlog2 = std::max<uint32_t>(11, ceil_log2(bound * 4 / 3 + 1));
   }
   const WarpLayout l = warp_layout(s);
@@ -982,7 +987,7 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);
   a.adja = ix.adja;
-  SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp);
+  SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp, a.n_live);
   SearchWs& ws = workspace(ix, st);
   std::lock_guard<std::mutex> ws_lock(ws.mu);
   DBufLite& tables = ws.tables;
@@ -1000,14 +1005,19 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
   launch(a, sh, ix.num_sms, st, tables, ~0ull);
-  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true, a.dp);
+  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true, a.dp, a.n_live);
+  // the retry grid's tables: at most ~1 GB (fewer resident warps for huge tables;
+  // the grid claims its overflowed queries dynamically, so any size is correct)
+  const uint64_t big_warp_bytes = 4ull << big.vlog2;
+  const uint64_t big_blocks = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ix.num_sms,
+                                                                       (1ull << 30) / (4 * big_warp_bytes)));
   SearchArgs b = a;
   b.qmap = a.ovf_list;
   b.nwork_dev = ovf;
   b.ovf_count = nullptr;  // cannot overflow: the table bounds every insert of max_iter iterations
   b.ovf_list = nullptr;
   b.work_ctr = a.work_ctr ? ctr + 1 : nullptr;
-  launch(b, big, ix.num_sms, st, big_tables, (uint64_t)ix.num_sms);
+  launch(b, big, ix.num_sms, st, big_tables, big_blocks);
   if (getenv("GRAB_DEBUG")) {
     uint32_t n_ovf = 0;
     GRAB_CUDA(cudaMemcpyAsync(&n_ovf, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));

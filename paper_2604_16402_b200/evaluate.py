@@ -25,7 +25,7 @@ from pathlib import Path
 import numpy as np
 
 from . import _lib as L
-from .api import brute_force_arrays, search_arrays
+from .api import brute_force_arrays, brute_force_search, search_arrays
 from .datasets import generate_ranges, recall_at_k
 from .params import SearchParams
 

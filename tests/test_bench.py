@@ -52,6 +52,8 @@ def test_bench_single_rank_line():
     assert d["steps"] == 3 and d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 6
     assert d["roofline"]["unit"] == "GB/s" and 0 < d["roofline"]["frac"]
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    # the CPU baseline (the reference's algorithm) returns the GPU's results exactly
+    assert d["cpu_baseline"]["result_agreement"] == 1.0
 
 
 @pytest.mark.gpu

@@ -1,0 +1,57 @@
+"""The reference package's OWN test-suite (pkg/tests, 73 tests) run against the
+drop-in: ``compat/bucketann`` aliases ``bucketann`` (and its submodules) to this
+package, so every ``from bucketann... import`` in those files resolves to the
+device implementation.
+
+The suite is copied (not committed) into ``baseline/_ref_tests`` by
+``tools/fetch_reference_tests.sh``; without the copy this test skips. Every
+failure must be listed in JUSTIFIED with the reason; anything else fails.
+"""
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUITE = os.path.join(ROOT, "baseline", "_ref_tests")
+
+# test id -> why the drop-in does not (and should not) pass it
+JUSTIFIED = {
+    "test_builder.py::test_global_graph_zero_rounds_is_init_plus_reverse_merge":
+        "imports the reference's private numpy helpers _random_init_graph / _reverse_merge_topk "
+        "(builder.py:270-335), which have no counterpart on the device path; the same property "
+        "(pass 2 with 0 rounds = random init + reverse merge) is pinned row for row against the "
+        "reference in tests/test_gpu_build.py::test_nn_descent_global_pass_matches_reference",
+}
+
+
+def test_reference_suite_passes_on_the_device_package(tmp_path):
+    if not os.path.isdir(SUITE) or not any(f.startswith("test_") for f in os.listdir(SUITE)):
+        pytest.skip("reference tests not fetched (tools/fetch_reference_tests.sh)")
+    xml = tmp_path / "ref.xml"
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "compat"), ROOT]),
+               PYTHONDONTWRITEBYTECODE="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", SUITE, "-q", "-p", "no:cacheprovider", "-o",
+                        "addopts=", "--rootdir", SUITE, f"--junitxml={xml}"],
+                       cwd=SUITE, env=env, capture_output=True, text=True, timeout=1200)
+    print(r.stdout[-4000:])
+    root = ET.parse(xml).getroot()
+    cases = list(root.iter("testcase"))
+    failed = {}
+    for c in cases:
+        bad = [e for e in c if e.tag in ("failure", "error")]
+        if bad:
+            tid = f"{c.get('classname').split('.')[-1]}.py::{c.get('name')}"
+            failed[tid] = (bad[0].get("message") or "")[:300]
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "reference_suite.log"), "w") as f:
+            f.write(r.stdout)
+    print(f"reference suite: {len(cases)} tests, {len(failed)} failed: {sorted(failed)}")
+    assert len(cases) >= 70
+    unexpected = {k: v for k, v in failed.items() if k not in JUSTIFIED}
+    assert not unexpected, unexpected
