@@ -64,6 +64,7 @@ __device__ __forceinline__ void list_insert(double* ld, uint32_t* ls, uint32_t k
     }
     __syncwarp();
   }
+  __syncwarp();  // every lane has read the list (no shift ran when pos == k - 1)
   if (lane == 0) {
     ld[pos] = d;
     ls[pos] = s;

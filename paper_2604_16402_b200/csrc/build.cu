@@ -232,6 +232,7 @@ __global__ void k_local_merge(const uint32_t* rows, uint64_t nrows, const uint32
       }
       __syncwarp();
     }
+    __syncwarp();  // every lane has read the list (no shift ran when pos == K - 1)
     if (lane == 0) {
       ld[pos] = d;
       ls[pos] = s;
@@ -319,6 +320,7 @@ __global__ void k_union_topk(const uint32_t* rows, uint64_t nrows, const uint32_
       }
       __syncwarp();
     }
+    __syncwarp();  // every lane has read the list (no shift ran when pos == K - 1)
     if (lane == 0) {
       ld[pos] = d;
       ls[pos] = s;

@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <map>
 #include <memory>
+#include <algorithm>
 #include <mutex>
 
 #include "index.cuh"
@@ -54,6 +55,49 @@ void upload_pcg_jump_tables() {
 
 __device__ __forceinline__ uint32_t hash32(uint32_t k) { return k * 0x9E3779B1u; }
 
+// Visited-table accesses (global, per-warp, L2-resident). The tables are
+// written (clears, atomics) and re-read throughout a query while the candidate
+// row stream sweeps L2; with default priority their dirty lines were evicted and
+// re-fetched mid-query (ncu: 1.31 GB of DRAM writes per cfg2 launch for a
+// read-only search). Every table access therefore carries an L2 evict_last
+// policy so the ~45 MB of live tables stay resident under the row stream
+// (-DGRAB_VIS_NO_HINT restores plain accesses for A/B).
+#ifndef GRAB_VIS_NO_HINT
+__device__ __forceinline__ uint64_t vis_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t vis_or(uint32_t* a, uint32_t v) {
+  uint32_t o;
+  asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
+               : "=r"(o) : "l"(a), "r"(v), "l"(vis_policy()) : "memory");
+  return o;
+}
+// (ptxas rejects .L2::cache_hint on atom.cas: the hash mode's CAS is plain; its
+// lines are kept hot by the hinted loads that probe them)
+__device__ __forceinline__ uint32_t vis_cas(uint32_t* a, uint32_t cmp, uint32_t v) { return atomicCAS(a, cmp, v); }
+__device__ __forceinline__ uint32_t vis_ld(const uint32_t* a) {
+  uint32_t o;  // .cg: the L2 copy (the atomics live there), never a stale L1 line
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(o) : "l"(a), "l"(vis_policy()) : "memory");
+  return o;
+}
+__device__ __forceinline__ void vis_clear(uint32_t* p, uint32_t n) {
+  const uint64_t pol = vis_policy();
+  for (uint32_t i = lane_id() * 4; i < n; i += 128)
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(p + i), "r"(0u), "l"(pol)
+                 : "memory");
+}
+#else
+__device__ __forceinline__ uint32_t vis_or(uint32_t* a, uint32_t v) { return atomicOr(a, v); }
+__device__ __forceinline__ uint32_t vis_cas(uint32_t* a, uint32_t cmp, uint32_t v) { return atomicCAS(a, cmp, v); }
+__device__ __forceinline__ uint32_t vis_ld(const uint32_t* a) { return *((volatile const uint32_t*)a); }
+__device__ __forceinline__ void vis_clear(uint32_t* p, uint32_t n) {
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (uint32_t i = lane_id() * 4; i < n; i += 128) *reinterpret_cast<uint4*>(p + i) = z;
+}
+#endif
+
 // Open-addressing set of 2^lg u32 entries (value key+1, 0 = empty).
 // Every probe loop is warp-uniform (all 32 lanes iterate until no lane has a
 // pending probe): a per-lane trip count would leave the warp diverged, and a
@@ -64,12 +108,12 @@ __device__ __forceinline__ bool set_insert_w(uint32_t* tab, uint32_t lg, uint32_
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
   const uint32_t v = key + 1;
-  uint32_t cur = active ? atomicCAS(tab + h, 0u, v) : 0u;
+  uint32_t cur = active ? vis_cas(tab + h, 0u, v) : 0u;
   bool pending = active && cur != 0u && cur != v;
   while (__any_sync(0xFFFFFFFFu, pending)) {
     if (pending) {
       h = (h + 1) & mask;
-      cur = atomicCAS(tab + h, 0u, v);
+      cur = vis_cas(tab + h, 0u, v);
       pending = cur != 0u && cur != v;
     }
   }
@@ -81,12 +125,12 @@ __device__ __forceinline__ bool set_contains_w(const uint32_t* tab, uint32_t lg,
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
   const uint32_t v = key + 1;
-  uint32_t cur = active ? *((volatile const uint32_t*)(tab + h)) : 0u;
+  uint32_t cur = active ? vis_ld(tab + h) : 0u;
   bool pending = active && cur != 0u && cur != v;
   while (__any_sync(0xFFFFFFFFu, pending)) {
     if (pending) {
       h = (h + 1) & mask;
-      cur = *((volatile const uint32_t*)(tab + h));
+      cur = vis_ld(tab + h);
       pending = cur != 0u && cur != v;
     }
   }
@@ -110,14 +154,14 @@ struct Visited {
   __device__ __forceinline__ bool contains_w(uint32_t key, bool active) const {
     if (bm) {
       const uint32_t o = key - base;
-      return active && (*((volatile const uint32_t*)(tab + (o >> 5))) >> (o & 31) & 1u);
+      return active && (vis_ld(tab + (o >> 5)) >> (o & 31) & 1u);
     }
     return set_contains_w(tab, lg, key, active);
   }
   __device__ __forceinline__ bool insert_w(uint32_t key, bool active) const {
     if (bm) {
       const uint32_t o = key - base;
-      return active && !(atomicOr(tab + (o >> 5), 1u << (o & 31)) >> (o & 31) & 1u);
+      return active && !(vis_or(tab + (o >> 5), 1u << (o & 31)) >> (o & 31) & 1u);
     }
     return set_insert_w(tab, lg, key, active);
   }
@@ -579,7 +623,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
       vis.base = __ldg(a.bstart + lo_b);
       vis.nbits = __ldg(a.bstart + hi_b) + __ldg(a.bcount + hi_b) - vis.base;
       vis.bm = vis.nbits <= (32u << vlg);
-      clear_words(vtab, vis.clear_words_n());
+      vis_clear(vtab, vis.clear_words_n());
       __syncwarp();
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
       const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
@@ -692,7 +736,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
 #pragma unroll
               for (int t = 0; t < EPL; ++t) {
                 const uint32_t o = v[t] - vis.base;
-                cur[t] = ((cand_bits >> t) & 1u) ? atomicOr(vtab + (o >> 5), 1u << (o & 31)) : 0u;
+                cur[t] = ((cand_bits >> t) & 1u) ? vis_or(vtab + (o >> 5), 1u << (o & 31)) : 0u;
               }
               if constexpr (STATS) count_unique();  // overlaps the visited atomics' round trip
 #pragma unroll
@@ -705,7 +749,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
 #pragma unroll
               for (int t = 0; t < EPL; ++t) {
                 h[t] = hash32(v[t]) >> (32 - vlg);
-                cur[t] = ((cand_bits >> t) & 1u) ? atomicCAS(vtab + h[t], 0u, v[t] + 1) : 0u;
+                cur[t] = ((cand_bits >> t) & 1u) ? vis_cas(vtab + h[t], 0u, v[t] + 1) : 0u;
               }
               uint32_t pend = 0;  // rare collisions: probe on, warp-uniformly
 #pragma unroll
@@ -716,7 +760,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
                 for (int t = 0; t < EPL; ++t) {
                   if ((pend >> t) & 1u) {
                     h[t] = (h[t] + 1) & vmask;
-                    cur[t] = atomicCAS(vtab + h[t], 0u, v[t] + 1);
+                    cur[t] = vis_cas(vtab + h[t], 0u, v[t] + 1);
                     if (cur[t] == 0u || cur[t] == v[t] + 1) pend &= ~(1u << t);
                   }
                 }
@@ -981,8 +1025,31 @@ static SearchWs& workspace(const DevIndex& ix, cudaStream_t st) {
   return *slot;
 }
 
+// The visited tables' evict_last accesses stay resident for good only inside
+// the L2 set-aside for persisting lines (0 by default). GRAB_L2_PERSIST=1
+// reserves the device maximum once per device: DRAM writes per cfg2 launch
+// 0.88 -> 0.07 GB and 10 % selectivity 4 % faster, but the set-aside crowds the
+// candidate rows out at wide ranges (50 %: 12 % slower), so it is opt-in.
+static void reserve_persisting_l2() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  GRAB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  done.push_back(dev);
+  if (!getenv("GRAB_L2_PERSIST")) return;  // opt-in: measured a net loss at wide ranges
+  int mx = 0;
+  if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || mx <= 0) return;
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (cur < (size_t)mx) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx);
+  cudaGetLastError();  // best effort: never fail a search over the cache reservation
+}
+
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
+  reserve_persisting_l2();
   if (a.width * a.k_max > 256) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 256 not supported");
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);

@@ -243,7 +243,7 @@ def test_append_batch_matches_oracle(g):
     ref, _, _ = construct.build(X[:2_000], S[:2_000], cfg, capacity=2_400)
     gi = g.load_index(ist.container_bytes(ref), g.BuildParams(k_max=16, k_local=8, bucket_capacity=500))
     ids = np.arange(9_000, 9_300, dtype=np.int64)
-    assert g.append_batch(gi, X[2_000:], S[2_000:], ids=ids) == (2_000, 2_300)
+    assert g.append_batch(gi, None, X[2_000:], S[2_000:], ids=ids) == (2_000, 2_300)
     assert ist.append_rows(ref, X[2_000:], S[2_000:], ids=ids) == (2_000, 2_300)
     assert gi.count == 2_300 and np.array_equal(gi.store.ids[2_000:2_300], ids)
     assert np.array_equal(gi.store.X[:2_300], ref.X[:2_300]) and np.array_equal(gi.store.scalars[:2_300],
@@ -253,9 +253,9 @@ def test_append_batch_matches_oracle(g):
     assert (gi.adjacency[2_000:2_300] == SENT).all()
     assert np.array_equal(gi.adjacency[:2_000], ref.adjacency[:2_000])
     with pytest.raises(g.CapacityError):
-        g.append_batch(gi, X[:200], S[:200])
+        g.append_batch(gi, None, X[:200], S[:200])
     with pytest.raises(g.DimensionMismatchError):
-        g.append_batch(gi, np.zeros((3, 8), np.float32), np.zeros(3, np.float32))
+        g.append_batch(gi, None, np.zeros((3, 8), np.float32), np.zeros(3, np.float32))
     # a graph-less append followed by a search: the appended rows are reachable only as seeds
     r = g.search_arrays(gi, X[2_100:2_110], 0.0, 1.0, g.SearchParams(k=10, itopk=64), seed_base=1)
     assert (r.counts == 10).all()

@@ -1,0 +1,36 @@
+"""compute-sanitizer gate: memcheck, racecheck and synccheck over a
+small workload that launches every kernel family (tools/sanitize_workload.py:
+build incl. the tcgen05 screen, search in bitmap / hash modes, brute force,
+insert / rewire / heal, append, phase-level ABI, SCC, sharded pack + merge).
+Each tool must report 0 errors; the logs go to gpurun_out/ for profiles/."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    env = dict(os.environ, GRAB_NO_ZERO_COPY="1")
+    cmd = [SAN, f"--tool={tool}", "--error-exitcode=97", "--print-limit=50", "--target-processes=all",
+           sys.executable, os.path.join(ROOT, "tools", "sanitize_workload.py")]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    logdir = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(logdir):
+        with open(os.path.join(logdir, f"sanitizer_{tool}.log"), "w") as f:
+            f.write(out)
+    assert "sanitize workload ok" in out, out[-3000:]
+    assert r.returncode == 0, out[-3000:]
+    clean = "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck" \
+        else "ERROR SUMMARY: 0 errors"
+    assert clean in out, out[-3000:]

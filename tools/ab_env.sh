@@ -1,0 +1,18 @@
+#!/bin/bash
+# A/B one library under two environments (alternating), plus one DRAM-bytes ncu
+# pass of each at the 10 % point:  ENVA="X=1" ENVB="" bash tools/ab_env.sh
+cd "$(dirname "$0")/.."
+PAIRS=${PAIRS:-0.01@400:4:150,0.1@296:4:100,0.5@464:4:150}
+for r in 1 2; do
+  for v in A B; do
+    E=ENV$v
+    echo "== $v (${!E}) round $r"; env ${!E} python tools/search_lab.py --config cfg2 --reps 10 --pairs $PAIRS 2>&1 | grep "stats="
+  done
+done
+for v in A B; do
+  E=ENV$v
+  env ${!E} ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
+      -k regex:k_search -s 2 -c 1 --csv python tools/search_lab.py --config cfg2 --reps 1 --pairs 0.1@296:4:100 \
+      > gpurun_out/ab_env_ncu_$v.csv 2>/dev/null
+  echo "== ncu $v"; grep -E "dram__bytes|gpu__time|hit_rate" gpurun_out/ab_env_ncu_$v.csv | awk -F'","' '{print $(NF-2), $(NF-1), $NF}'
+done
