@@ -424,12 +424,26 @@ __device__ __forceinline__ uint32_t admit(uint4* qe, double* cd, uint32_t* cs, u
     // final position of survivor i: i + (queue entries before it); distinct and increasing
     const uint32_t f = lane < cnt ? lane + rank_in_queue(qe, L, d, s) : kFull;
     const uint32_t f0 = __shfl_sync(kFull, f, 0);
+    const uint32_t flast = __shfl_sync(kFull, f, cnt - 1);
     const uint32_t newL = min(itopk, L + cnt);
     // fill the output positions [f0, newL) chunk by chunk from the top: position
     // pos holds survivor (#survivors before pos) if some f == pos, else queue
     // entry pos - (#survivors before pos); every source index is <= pos, so
     // top-down chunks read their sources before anything below is written
-    for (int32_t c0 = (int32_t)((newL - 1) & ~31u); c0 >= (int32_t)(f0 & ~31u); c0 -= 32) {
+    int32_t c0 = (int32_t)((newL - 1) & ~31u);
+    // chunks above the last survivor are a plain shift by cnt (one LDS.128 +
+    // STS.128 per entry): a chunk's reads [P0 - cnt, P0 + 31] never overlap the
+    // writes of the chunks above it, so one __syncwarp (read before write inside
+    // the chunk) is all the ordering it needs
+    for (; c0 > (int32_t)flast; c0 -= 32) {
+      const uint32_t pos = (uint32_t)c0 + lane;
+      uint4 e = make_uint4(0, 0, 0, 0);
+      if (pos < newL) e = qe[pos - cnt];
+      __syncwarp();
+      if (pos < newL) qe[pos] = e;
+    }
+    __syncwarp();
+    for (; c0 >= (int32_t)(f0 & ~31u); c0 -= 32) {
       const uint32_t P0 = (uint32_t)c0, pos = P0 + lane;
       const uint32_t B = __reduce_or_sync(kFull, (f >= P0 && f < P0 + 32) ? 1u << (f - P0) : 0u);
       const uint32_t before = __popc(__ballot_sync(kFull, f < P0)) + __popc(B & ((1u << lane) - 1));
@@ -883,7 +897,7 @@ static uint32_t ceil_log2(uint64_t x) {
 }
 
 SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst,
-                       uint32_t dp, uint64_t live_rows) {
+                       uint32_t dp, uint64_t live_rows, bool stats) {
   SearchShape s;
   const uint32_t nc = (dp + 127) / 128;
   s.qbytes = nc > 2 ? (nc <= 4 ? 4u : nc <= 8 ? 8u : 16u) * 512u : 0u;  // QueryRegs<NC>::kShared staging
@@ -891,7 +905,10 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
   s.width = width;
   const uint32_t fan = width * k_max;
   s.cmax = 1u << ceil_log2(std::max<uint64_t>(std::max(fan, want), 32));  // bitonic pads to a power of 2
-  s.dsz = 1u << ceil_log2(std::max<uint64_t>(4ull * fan, 128));  // dedup table, load <= 1/4
+  // dedup table, load <= 1/4; it only exists for the SearchStats counters: the
+  // stats-free instance keeps just the 64-word seed stage that shares it (2 KB
+  // less shared memory per warp at width 4: 5 -> 6 blocks per SM at itopk 400)
+  s.dsz = stats ? 1u << ceil_log2(std::max<uint64_t>(4ull * fan, 128)) : 64u;
   if (!worst) {
     // sized for the visits of a wide (hash-mode) search: ~itopk * 36 at full range (1M rows, itopk 128:
     // a 4K table overflowed every insert candidate search); a bitmap needs only nbits / 8 of it
@@ -1054,7 +1071,8 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);
   a.adja = ix.adja;
-  SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp, a.n_live);
+  SearchShape sh = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, false, a.dp, a.n_live,
+                              a.out_stats != nullptr);
   SearchWs& ws = workspace(ix, st);
   std::lock_guard<std::mutex> ws_lock(ws.mu);
   DBufLite& tables = ws.tables;
@@ -1072,7 +1090,8 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
   launch(a, sh, ix.num_sms, st, tables, ~0ull);
-  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true, a.dp, a.n_live);
+  SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true, a.dp, a.n_live,
+                               a.out_stats != nullptr);
   // the retry grid's tables: at most ~1 GB (fewer resident warps for huge tables;
   // the grid claims its overflowed queries dynamically, so any size is correct)
   const uint64_t big_warp_bytes = 4ull << big.vlog2;

@@ -1,6 +1,7 @@
 """Build a config on the GPU and run the search kernel a few times (for ncu / timing).
 
-    ncu --set full -k regex:k_search -s 2 -c 1 -o gpurun_out/search python tools/profile_search.py --config cfg2
+    ncu --set full --profile-from-start off -k regex:k_search -c 1 -o gpurun_out/search \
+        python tools/profile_search.py --config cfg2
     python tools/profile_search.py --config cfg2 --time        # QPS + recall per operating point
 """
 import argparse
@@ -25,6 +26,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--points", default="")
 ap.add_argument("--sel", type=float, default=0.1)
+ap.add_argument("--nostats", action="store_true", help="profile the stats-free kernel instance")
 a = ap.parse_args()
 n, dim, cap, nq, itopk, width, iters = P[a.config]
 itopk = a.itopk or itopk
@@ -55,7 +57,15 @@ for it_, w_, mi_ in points:
         dt = (time.perf_counter() - t0) / a.reps
         print(f"itopk {it_} width {w_} iters {mi_}: recall {rec:.4f} qps {nq / dt:,.0f} ({dt * 1e3:.2f} ms/batch)")
     else:
-        for _ in range(a.reps):
-            r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0)
+        import torch
+        for rep_ in range(a.reps):
+            if rep_ == a.reps - 1:  # ncu --profile-from-start off: only the last rep is captured
+                torch.cuda.synchronize()
+                torch.cuda.profiler.start()
+            r = g.search_arrays(gi, Q, lo, hi, sp, seed_base=0, stats=not a.nostats)
+            if rep_ == a.reps - 1:
+                torch.cuda.synchronize()
+                torch.cuda.profiler.stop()
         st = r.stats
-        print("mean stats:", {f: float(np.mean(st[f])) for f in st.dtype.names})
+        if st is not None:
+            print("mean stats:", {f: float(np.mean(st[f])) for f in st.dtype.names})
