@@ -3,6 +3,8 @@
 #pragma once
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "index.cuh"
 
 namespace grab {
@@ -23,6 +25,25 @@ struct KnnJob {
 void knn_device(const DevIndex& ix, const float* norms, const std::vector<KnnJob>& jobs, uint32_t K, bool tb_slot,
                 uint32_t* out_ids, double* out_d, cudaStream_t st, bool causal = false);
 void row_norms(const DevIndex& ix, float* out, cudaStream_t st);
+
+// Brute-force mode of the tcgen05 screen (knn_tc.cu k_knn_screen_tc<true>).
+struct TcBf {
+  const float* qnorm = nullptr;    // [ntile * 128] |q|^2 of the sorted query rows
+  const float* qlo = nullptr;      // [ntile * 128] f32 bounds (lo > hi: no range)
+  const float* qhi = nullptr;
+  const uint32_t* span = nullptr;  // [ntile][2] phys column span of each query tile
+  uint32_t S = 1;                  // column splits (CTAs) per tile
+  uint64_t* keys = nullptr;        // [ntile * S][128][KP] heap entries, root = kept max, ~0 = empty
+};
+// keys per (query tile, split) of the split-BF16 screen of the sorted query
+// rows q_hi / q_lo ([ntile * 128] x kp) against the index's live columns
+// (masked_norms: |x|^2 per phys row, +inf for rows that are not live, padded to
+// a whole column tile past phys_cap plus one: div_up(phys_cap, 64) * 64 + 64)
+// x_hi / x_lo: the same split of the phys rows ([phys_cap] x kp)
+void bf_screen_tc(const DevIndex& ix, const __nv_bfloat16* q_hi, const __nv_bfloat16* q_lo, const __nv_bfloat16* x_hi,
+                  const __nv_bfloat16* x_lo, uint32_t ntile, const float* masked_norms, uint32_t KP, TcBf bf,
+                  cudaStream_t st);
+uint32_t tc_pad_cols();
 
 // tcgen05 split-BF16 screen (knn_tc.cu): same output contract as the SIMT screen
 // (per query row, KP candidate phys ids in cand[row * KP ..]).

@@ -146,14 +146,24 @@ struct Smem {
 
 constexpr uint32_t kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 
+// BF = true: the batched brute-force screen (bf_screen_tc). The A tile is 128
+// range queries (sorted by slab start, tmap over their hi/lo split), the B
+// stream is the phys columns of the tile's span [span[2t], span[2t+1]) split
+// S ways (CTA (t, s) takes column tiles s, s+S, ...), every column is checked
+// against the row's own f32 range, and the CTA writes each row's raw heap
+// (root = the kept maximum, ~0 = empty) to keys[(cta * BM + row) * KP ..].
+template <bool BF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_knn_screen_tc(const __grid_constant__ CUtensorMap tmap_ahi, const __grid_constant__ CUtensorMap tmap_alo,
                     const __grid_constant__ CUtensorMap tmap_bhi, const __grid_constant__ CUtensorMap tmap_blo,
                     const KnnJob* jobs, const Attr* attr, const float* row_norms, const float* norms,
                     uint32_t nkc, uint32_t KP, uint32_t* cand, int causal, uint32_t STAGES, uint32_t NG,
-                    int stream_a) {
+                    int stream_a, const TcBf bf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // aligned by an offset from the shared array (not an integer round trip), so
+  // the compiler keeps the shared address space: the heaps compile to LDS/STS,
+  // not generic loads with an address-space conversion each
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // resident A (d <= 128): A hi/lo for every K chunk loaded once, the ring holds
   // one column tile's B hi/lo (all K chunks) per stage. Streamed A (d > 128):
   // every ring stage holds ONE K chunk of A hi/lo and B hi/lo, so any d fits and
@@ -173,9 +183,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
 
-  const KnnJob job = jobs[blockIdx.x];
+  uint32_t r0, nr, c0, c1, split = 0, S = 1;
+  if constexpr (BF) {
+    const uint32_t tile = blockIdx.x / bf.S;
+    split = blockIdx.x % bf.S;
+    S = bf.S;
+    r0 = tile * BM;
+    nr = BM;
+    c0 = bf.span[2 * tile];
+    c1 = bf.span[2 * tile + 1];
+    if (c1 < c0) c1 = c0;  // no live query in the tile
+  } else {
+    const KnnJob job = jobs[blockIdx.x];
+    r0 = job.r0;
+    nr = job.nr;
+    c0 = job.c0;
+    c1 = job.c1;
+  }
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t ntiles = (job.c1 - job.c0 + BN - 1) / BN;
+  const uint32_t nct = (c1 - c0 + BN - 1) / BN;  // column tiles of the span
+  const uint32_t ntiles = nct > split ? (nct - split + S - 1) / S : 0;  // this CTA's share
+  // first column of this CTA's t-th column tile
+  auto col_of = [&](uint32_t t) -> uint32_t { return c0 + (split + t * S) * BN; };
 
   if (threadIdx.x == 0) {
     mbar_init(a_full, 1);
@@ -206,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- TMA producer, streamed A: ring slot u = (tile t, K chunk c)
       uint32_t u = 0;
       for (uint32_t t = 0; t < ntiles; ++t) {
-        const int32_t row = (int32_t)(job.c0 + t * BN);
+        const int32_t row = (int32_t)col_of(t);
         for (uint32_t c = 0; c < nkc; ++c, ++u) {
           const uint32_t s = u % STAGES, round = u / STAGES;
           mbar_wait(b_empty + s, (round & 1) ^ 1);
@@ -215,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* bh = al + Smem::kChunkA;
           uint8_t* bl = bh + Smem::kChunkB;
           mbar_expect_tx(b_full + s, st_bytes);
-          tma_load_2d(ah, &tmap_ahi, b_full + s, (int32_t)(c * KCH), (int32_t)job.r0);
-          tma_load_2d(al, &tmap_alo, b_full + s, (int32_t)(c * KCH), (int32_t)job.r0);
+          tma_load_2d(ah, &tmap_ahi, b_full + s, (int32_t)(c * KCH), (int32_t)r0);
+          tma_load_2d(al, &tmap_alo, b_full + s, (int32_t)(c * KCH), (int32_t)r0);
           tma_load_2d(bh, &tmap_bhi, b_full + s, (int32_t)(c * KCH), row);
           tma_load_2d(bl, &tmap_blo, b_full + s, (int32_t)(c * KCH), row);
         }
@@ -253,8 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- TMA producer
       mbar_expect_tx(a_full, 2 * a_bytes);
       for (uint32_t c = 0; c < nkc; ++c) {
-        tma_load_2d(A_hi + c * Smem::kChunkA, &tmap_ahi, a_full, (int32_t)(c * KCH), (int32_t)job.r0);
-        tma_load_2d(A_lo + c * Smem::kChunkA, &tmap_alo, a_full, (int32_t)(c * KCH), (int32_t)job.r0);
+        tma_load_2d(A_hi + c * Smem::kChunkA, &tmap_ahi, a_full, (int32_t)(c * KCH), (int32_t)r0);
+        tma_load_2d(A_lo + c * Smem::kChunkA, &tmap_alo, a_full, (int32_t)(c * KCH), (int32_t)r0);
       }
       for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t s = t % STAGES, round = t / STAGES;
@@ -262,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* bh = B + s * 2 * b_bytes;
         uint8_t* bl = bh + b_bytes;
         mbar_expect_tx(b_full + s, 2 * b_bytes);
-        const int32_t row = (int32_t)(job.c0 + t * BN);
+        const int32_t row = (int32_t)col_of(t);
         for (uint32_t c = 0; c < nkc; ++c) {
           tma_load_2d(bh + c * Smem::kChunkB, &tmap_bhi, b_full + s, (int32_t)(c * KCH), row);
           tma_load_2d(bl + c * Smem::kChunkB, &tmap_blo, b_full + s, (int32_t)(c * KCH), row);
@@ -307,10 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // tile's columns and a private heap per row (merged at the end).
     const uint32_t e = warp - 2, sub = warp & 3, grp = e >> 2;
     const uint32_t r = sub * 32 + lane;
-    const uint32_t prow = job.r0 + r;
+    const uint32_t prow = r0 + r;
     const bool active = grp < NG;
-    const bool row_ok = active && r < job.nr && attr[prow].slot != kNoSlot;
-    const float a2 = row_ok ? row_norms[prow] : 0.f;
+    float qlo = 0.f, qhi = 0.f;
+    bool row_ok;
+    if constexpr (BF) {
+      qlo = bf.qlo[prow];
+      qhi = bf.qhi[prow];
+      row_ok = active && qlo <= qhi;  // padding rows and empty ranges carry lo > hi
+    } else {
+      row_ok = active && r < nr && attr[prow].slot != kNoSlot;
+    }
+    const float a2 = row_ok ? (BF ? bf.qnorm[prow] : row_norms[prow]) : 0.f;
     uint64_t* h = H + grp * BM * KP + r;  // interleaved: element i at h[i * BM]
     uint64_t top = ~0ull;
     const uint32_t QN = 4 / NG;  // 16-column chunks per warp per tile
@@ -332,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + as);
       {  // every lane runs the chunk loop (the insertion pass below is warp-synchronous)
-        const uint32_t cb = job.c0 + t * BN + col0;
+        const uint32_t cb = col_of(t) + col0;
         // |b|^2 with +inf for headroom rows / past the tile's end (one broadcast
         // float4 load per 4 columns); the heap key is only built for survivors
         // of an f32 threshold test against the current K'-th distance.
@@ -358,11 +395,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           // admissible survivors of this chunk (finite, not the row itself, in
           // range, causal for insert candidates)
           uint32_t pend = 0;
+          if constexpr (BF) {
+            // the row's own range on the column's scalar: lane j loads column j's
+            // scalar once and the 16 are shuffled to every row (lane); n_live /
+            // headroom columns already carry +inf norms
+            const uint32_t cl = cb + q * 16 + (lane & 15);
+            const float scl = cl < c1 ? __ldg(&attr[cl].s) : __int_as_float(0x7FC00000);
 #pragma unroll
-          for (uint32_t j = 0; j < 16; ++j) {
-            const uint32_t c = cb + q * 16 + j;
-            pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && d[j] < INFINITY && c != prow && c < job.c1 &&
-                               !(causal && c > prow)) << j;
+            for (uint32_t j = 0; j < 16; ++j) {
+              const float sc = __shfl_sync(0xFFFFFFFFu, scl, j);  // NaN past c1: fails both tests
+              pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && d[j] < INFINITY && sc >= qlo && sc <= qhi) << j;
+            }
+          } else {
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+              const uint32_t c = cb + q * 16 + j;
+              pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && d[j] < INFINITY && c != prow && c < c1 &&
+                                 !(causal && c > prow)) << j;
+            }
           }
           // heap insertions lane-parallel: every lane takes its NEXT survivor in
           // the same pass, so a pass costs one sift-down for all lanes at once
@@ -387,6 +437,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // merge the column groups' heaps (group 0 absorbs group 1), then emit
     asm volatile("bar.sync 1, %0;" ::"r"(kThreads - 64));
+    if (BF && !row_ok && grp == 0 && active) {
+      for (uint32_t i = 0; i < KP; ++i) bf.keys[((uint64_t)blockIdx.x * BM + r) * KP + i] = ~0ull;
+    }
     if (row_ok && grp == 0) {
       for (uint32_t g = 1; g < NG; ++g) {
         const uint64_t* o = H + g * BM * KP + r;
@@ -398,8 +451,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      for (uint32_t i = 0; i < KP; ++i)
-        cand[(uint64_t)prow * KP + i] = h[i * BM] == ~0ull ? kSentinel : (uint32_t)h[i * BM];
+      if constexpr (BF) {
+        for (uint32_t i = 0; i < KP; ++i) bf.keys[((uint64_t)blockIdx.x * BM + r) * KP + i] = h[i * BM];
+      } else {
+        for (uint32_t i = 0; i < KP; ++i)
+          cand[(uint64_t)prow * KP + i] = h[i * BM] == ~0ull ? kSentinel : (uint32_t)h[i * BM];
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -502,13 +559,57 @@ void knn_screen_tc(const DevIndex& ix, const float* norms, const KnnJob* djobs, 
     }
   }
   if (!stages) throw Error(GRAB_ERR_VALUE, "tensor-core kNN tile exceeds shared memory");
-  GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_knn_screen_tc<<<njobs, kThreads, smem, st>>>(ahi, alo, bhi, blo, djobs, ix.attr, norms, nm, nkc, KP, cand,
-                                                 causal ? 1 : 0, stages, ng, stream_a);
+  GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_knn_screen_tc<false><<<njobs, kThreads, smem, st>>>(ahi, alo, bhi, blo, djobs, ix.attr, norms, nm, nkc, KP, cand,
+                                                        causal ? 1 : 0, stages, ng, stream_a, TcBf{});
   GRAB_CHECK_LAUNCH();
   GRAB_CUDA(cudaFreeAsync(nm, st));
   GRAB_CUDA(cudaFreeAsync(hi, st));
   GRAB_CUDA(cudaFreeAsync(lo, st));
 }
+
+// ring depth / column groups for a screen launch (shared by both modes)
+static void tc_config(uint32_t nkc, int stream_a, uint32_t KP, uint32_t& stages, uint32_t& ng, size_t& smem) {
+  using namespace tc;
+  stages = 0;
+  ng = 0;
+  for (uint32_t g = 2; g >= 1 && !stages; --g) {
+    for (uint32_t s = MAX_STAGES; s >= 2; --s) {
+      const size_t ring = stream_a ? s * 2 * (size_t)(Smem::kChunkA + Smem::kChunkB)
+                                   : 2 * (size_t)nkc * BM * 128 + s * 2 * (size_t)nkc * BN * 128;
+      const size_t b = 1024 + ring + (size_t)g * BM * KP * 8 + 16 * 8;
+      if (b <= 227 * 1024) {
+        stages = s;
+        ng = g;
+        smem = b;
+        break;
+      }
+    }
+  }
+  if (!stages) throw Error(GRAB_ERR_VALUE, "tensor-core kNN tile exceeds shared memory");
+}
+
+void bf_screen_tc(const DevIndex& ix, const __nv_bfloat16* q_hi, const __nv_bfloat16* q_lo, const __nv_bfloat16* hi,
+                  const __nv_bfloat16* lo, uint32_t ntile, const float* masked_norms, uint32_t KP, TcBf bf,
+                  cudaStream_t st) {
+  using namespace tc;
+  const uint32_t kp = (ix.dp + KCH - 1) / KCH * KCH;
+  const uint32_t nkc = kp / KCH;
+  const uint64_t rows = ix.phys_cap;
+  const uint64_t qrows = (uint64_t)ntile * BM;
+  const CUtensorMap ahi = make_map((void*)q_hi, qrows, kp, BM), alo = make_map((void*)q_lo, qrows, kp, BM);
+  const CUtensorMap bhi = make_map((void*)hi, rows, kp, BN), blo = make_map((void*)lo, rows, kp, BN);
+  const int stream_a = kp > 128 ? 1 : 0;
+  uint32_t stages, ng;
+  size_t smem;
+  tc_config(nkc, stream_a, KP, stages, ng, smem);
+  GRAB_CUDA(cudaFuncSetAttribute(k_knn_screen_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_knn_screen_tc<true><<<ntile * bf.S, kThreads, smem, st>>>(ahi, alo, bhi, blo, nullptr, ix.attr, nullptr,
+                                                              masked_norms, nkc, KP, nullptr, 0, stages, ng, stream_a,
+                                                              bf);
+  GRAB_CHECK_LAUNCH();
+}
+
+uint32_t tc_pad_cols() { return tc::BN; }
 
 }  // namespace grab
