@@ -464,12 +464,58 @@ class InsertReport:
     evictions_necessary: int = 0
     evictions_redundant: int = 0
     forced_links: int = 0
-    rewired_rows: list = field(default_factory=list)
+    rewired_rows: Sequence = field(default_factory=list)
     wall_time_s: float = 0.0
     phase_seconds: dict = field(default_factory=dict)
 
     def to_dict(self) -> dict:
-        return dict(self.__dict__)
+        d = dict(self.__dict__)
+        if isinstance(d["rewired_rows"], RowList):
+            d["rewired_rows"] = d["rewired_rows"].tolist()
+        return d
+
+
+class RowList(Sequence):
+    """InsertReport.rewired_rows (updater.py:42,261: a sorted list of slots),
+    backed by the library's uint32 array: building a Python list of ~1M ints
+    cost more than the device work of a 100K batch. Compares equal to a list
+    with the same items; ``tolist()`` / ``np.asarray`` give the plain forms."""
+
+    __slots__ = ("_a",)
+
+    def __init__(self, a: np.ndarray):
+        self._a = a
+
+    def __len__(self) -> int:
+        return len(self._a)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return self._a[i].astype(np.int64).tolist()
+        return int(self._a[i])
+
+    def __iter__(self):
+        return iter(self._a.astype(np.int64).tolist())
+
+    def __contains__(self, v) -> bool:
+        i = int(np.searchsorted(self._a, v))
+        return i < len(self._a) and int(self._a[i]) == v
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, RowList):
+            return np.array_equal(self._a, other._a)
+        if isinstance(other, (list, tuple, np.ndarray)):
+            return len(other) == len(self._a) and np.array_equal(self._a, np.asarray(other))
+        return NotImplemented
+
+    def __array__(self, dtype=None, copy=None):
+        return self._a.astype(dtype or np.int64)
+
+    def tolist(self) -> list:
+        return self._a.astype(np.int64).tolist()
+
+    def __repr__(self) -> str:
+        return f"RowList({self._a.tolist()!r})" if len(self._a) <= 20 else f"RowList(<{len(self._a)} rows>)"
 
 
 _INSERT_PHASES = ["append", "bucket_candidates", "candidate_search", "forward_select", "reverse_rewire", "heal"]
@@ -523,7 +569,7 @@ def insert_batch(index: GraphIndex, vectors, scalars, *, ids=None, search_itopk:
                         reverse_accepted=int(rep.reverse_accepted), reverse_rejected=int(rep.reverse_rejected),
                         evictions_necessary=int(rep.evictions_necessary),
                         evictions_redundant=int(rep.evictions_redundant), forced_links=int(rep.forced_links),
-                        rewired_rows=rw.astype(np.int64).tolist(), wall_time_s=float(rep.wall_time_s),
+                        rewired_rows=RowList(rw), wall_time_s=float(rep.wall_time_s),
                         phase_seconds={k: float(rep.phase_seconds[i]) for i, k in enumerate(_INSERT_PHASES)})
 
 

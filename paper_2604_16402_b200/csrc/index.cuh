@@ -68,6 +68,7 @@ struct DevIndex {
 
   // buckets
   uint32_t m = 0;
+  uint32_t m_alloc = 0;        // bucket count the device tables below are sized for
   float* bound = nullptr;      // [m+1]
   uint32_t* bstart = nullptr;  // [m]
   uint32_t* bcount = nullptr;  // [m]

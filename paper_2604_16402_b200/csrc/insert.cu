@@ -17,6 +17,7 @@
 // the whole batch in parallel without changing the result.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -313,6 +314,27 @@ __global__ void k_req_heads(const unsigned long long* keys, uint64_t n, uint8_t*
   if (i >= n) return;
   head[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
 }
+
+// Sorted keys with an all-ones padding suffix: *nvalid = length of the valid
+// prefix (the one index whose successor is padding), and head[i] = 1 where a
+// run of equal high 32 bits starts inside that prefix (0 elsewhere).
+__global__ void k_valid_heads(const unsigned long long* keys, uint64_t n, uint8_t* head, uint32_t* nvalid) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool v = keys[i] != ~0ull;
+  if (v && (i + 1 == n || keys[i + 1] == ~0ull)) *nvalid = (uint32_t)(i + 1);
+  if (i == 0 && !v) *nvalid = 0;
+  head[i] = v && (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+}
+
+struct IsZero {
+  const uint32_t* c;
+  __host__ __device__ bool operator()(uint32_t i) const { return c[i] == 0; }
+};
+struct IsSet {
+  const uint8_t* f;
+  __host__ __device__ bool operator()(uint32_t i) const { return f[i] != 0; }
+};
 
 // Distances from the row in `r` to row entries j0 .. j0+G-1 of a lane-distributed
 // row (entry j held by lane j % 32 in e[j / 32]), G = Batch<NC>::G rows in
@@ -624,40 +646,27 @@ __global__ void k_heal_apply(const unsigned long long* keys, uint64_t nreq, cons
 }
 
 // Sorted u64 keys (valid prefix, ~0 padding) -> number of valid keys and the
-// start index of every run with equal high 32 bits.
+// start index of every run with equal high 32 bits (one host round trip).
 static uint64_t segment_heads(Pool& pool, const unsigned long long* keys, uint64_t n, uint32_t** heads_out,
                               uint32_t* nheads_out, cudaStream_t st) {
-  uint64_t lo = 0, hi = n;
-  unsigned long long probe = 0;
-  while (lo < hi) {
-    uint64_t mid = (lo + hi) / 2;
-    GRAB_CUDA(cudaMemcpyAsync(&probe, keys + mid, 8, cudaMemcpyDeviceToHost, st));
-    GRAB_CUDA(cudaStreamSynchronize(st));
-    if (probe == ~0ull)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  const uint64_t nv = lo;
   *nheads_out = 0;
-  if (!nv) return 0;
-  uint8_t* head = pool.alloc<uint8_t>(nv);
-  k_req_heads<<<(unsigned)div_up(nv, 256), 256, 0, st>>>(keys, nv, head);
+  if (!n) return 0;
+  uint8_t* head = pool.alloc<uint8_t>(n);
+  uint32_t* cnts = pool.alloc<uint32_t>(2);  // {nvalid, nheads}
+  k_valid_heads<<<(unsigned)div_up(n, 256), 256, 0, st>>>(keys, n, head, cnts);
   GRAB_CHECK_LAUNCH();
-  uint32_t* idx = pool.alloc<uint32_t>(nv);
-  std::vector<uint32_t> seq(nv);
-  for (uint64_t i = 0; i < nv; ++i) seq[i] = (uint32_t)i;
-  GRAB_CUDA(cudaMemcpyAsync(idx, seq.data(), nv * 4, cudaMemcpyHostToDevice, st));
-  uint32_t* heads = pool.alloc<uint32_t>(nv);
-  uint32_t* nh = pool.alloc<uint32_t>(1);
+  uint32_t* heads = pool.alloc<uint32_t>(n);
+  cub::CountingInputIterator<uint32_t> idx(0);
   size_t tmp = 0;
-  cub::DeviceSelect::Flagged(nullptr, tmp, idx, head, heads, nh, (int)nv, st);
+  cub::DeviceSelect::Flagged(nullptr, tmp, idx, head, heads, cnts + 1, (int)n, st);
   void* t = pool.alloc<uint8_t>(tmp);
-  GRAB_CUDA(cub::DeviceSelect::Flagged(t, tmp, idx, head, heads, nh, (int)nv, st));
-  GRAB_CUDA(cudaMemcpyAsync(nheads_out, nh, 4, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cub::DeviceSelect::Flagged(t, tmp, idx, head, heads, cnts + 1, (int)n, st));
+  uint32_t hc[2];
+  GRAB_CUDA(cudaMemcpyAsync(hc, cnts, 8, cudaMemcpyDeviceToHost, st));
   GRAB_CUDA(cudaStreamSynchronize(st));
   *heads_out = heads;
-  return nv;
+  *nheads_out = hc[1];
+  return hc[0];
 }
 
 static unsigned long long* sort_keys(Pool& pool, unsigned long long* keys, uint64_t n, cudaStream_t st) {
@@ -898,36 +907,12 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
     cub::DeviceRadixSort::SortPairs(nullptr, tmp, req_key, k2, req_d, d2, (int)nr_all, 0, 64, st);
     void* t = pool.alloc<uint8_t>(tmp);
     GRAB_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, req_key, k2, req_d, d2, (int)nr_all, 0, 64, st));
-    // valid requests are the prefix (unused entries are all-ones keys)
-    std::vector<unsigned long long> probe(1);
-    uint64_t lo = 0, hi = nr_all;  // first invalid index by binary search on the device array
-    while (lo < hi) {
-      uint64_t mid = (lo + hi) / 2;
-      GRAB_CUDA(cudaMemcpyAsync(probe.data(), k2 + mid, 8, cudaMemcpyDeviceToHost, st));
-      GRAB_CUDA(cudaStreamSynchronize(st));
-      if (probe[0] == ~0ull)
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    const uint64_t nreq = lo;
+    // valid requests are the prefix (unused entries are all-ones keys): its length
+    // and the per-target run heads in one pass, one host round trip for both counts
+    uint32_t* heads = nullptr;
+    uint32_t nheads = 0;
+    const uint64_t nreq = segment_heads(pool, k2, nr_all, &heads, &nheads, st);
     if (nreq) {
-      uint8_t* head = pool.alloc<uint8_t>(nreq);
-      k_req_heads<<<(unsigned)div_up(nreq, 256), 256, 0, st>>>(k2, nreq, head);
-      GRAB_CHECK_LAUNCH();
-      uint32_t* idx = pool.alloc<uint32_t>(nreq);
-      uint32_t* heads = pool.alloc<uint32_t>(nreq);
-      uint32_t* nheads_d = pool.alloc<uint32_t>(1);
-      std::vector<uint32_t> seq(nreq);
-      for (uint64_t i = 0; i < nreq; ++i) seq[i] = (uint32_t)i;
-      GRAB_CUDA(cudaMemcpyAsync(idx, seq.data(), nreq * 4, cudaMemcpyHostToDevice, st));
-      size_t tmp2 = 0;
-      cub::DeviceSelect::Flagged(nullptr, tmp2, idx, head, heads, nheads_d, (int)nreq, st);
-      void* t2 = pool.alloc<uint8_t>(tmp2);
-      GRAB_CUDA(cub::DeviceSelect::Flagged(t2, tmp2, idx, head, heads, nheads_d, (int)nreq, st));
-      uint32_t nheads = 0;
-      GRAB_CUDA(cudaMemcpyAsync(&nheads, nheads_d, 4, cudaMemcpyDeviceToHost, st));
-      GRAB_CUDA(cudaStreamSynchronize(st));
       const uint32_t wpb = 4;
       by_nc(ix.dp, [&](auto ncv) {
         constexpr int NC = decltype(ncv)::value;
@@ -944,20 +929,29 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
     uint32_t* counts = pool.alloc<uint32_t>(b);
     uint32_t* miss = pool.alloc<uint32_t>(b);
     unsigned long long* hkeys = pool.alloc<unsigned long long>(b);
+    uint32_t* nmiss_d = pool.alloc<uint32_t>(1);
+    void* sel_tmp = nullptr;
+    size_t sel_tmp_bytes = 0;
     for (int round = 0; round < 4; ++round) {
       GRAB_CUDA(cudaMemsetAsync(counts, 0, b * 4, st));
       k_prefix_indeg<<<(unsigned)div_up(start * K, 256), 256, 0, st>>>(ix.adj, ix.slot2phys, ix.attr, start, K, start,
                                                                        end, counts);
       GRAB_CHECK_LAUNCH();
-      std::vector<uint32_t> hc(b);
-      GRAB_CUDA(cudaMemcpyAsync(hc.data(), counts, b * 4, cudaMemcpyDeviceToHost, st));
+      // newcomers without an in-edge from the prefix, compacted on the device
+      {
+        cub::CountingInputIterator<uint32_t> idx(0);
+        size_t tmp = 0;
+        cub::DeviceSelect::If(nullptr, tmp, idx, miss, nmiss_d, (int)b, IsZero{counts}, st);
+        if (tmp > sel_tmp_bytes) {
+          sel_tmp = pool.alloc<uint8_t>(tmp);
+          sel_tmp_bytes = tmp;
+        }
+        GRAB_CUDA(cub::DeviceSelect::If(sel_tmp, tmp, idx, miss, nmiss_d, (int)b, IsZero{counts}, st));
+      }
+      uint32_t nm = 0;
+      GRAB_CUDA(cudaMemcpyAsync(&nm, nmiss_d, 4, cudaMemcpyDeviceToHost, st));
       GRAB_CUDA(cudaStreamSynchronize(st));
-      std::vector<uint32_t> m;
-      for (uint64_t i = 0; i < b; ++i)
-        if (hc[i] == 0) m.push_back((uint32_t)i);
-      if (m.empty()) break;
-      const uint32_t nm = (uint32_t)m.size();
-      GRAB_CUDA(cudaMemcpyAsync(miss, m.data(), nm * 4, cudaMemcpyHostToDevice, st));
+      if (nm == 0) break;
       by_nc(ix.dp, [&](auto ncv) {
         constexpr int NC = decltype(ncv)::value;
         k_heal_choose<NC><<<(unsigned)div_up(nm, 4), 128, 0, st>>>(miss, nm, start, ix.slot2phys, ix.attr, ix.X,
@@ -981,11 +975,21 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
   mark(5);
   InsertCounters hcnt;
   GRAB_CUDA(cudaMemcpyAsync(&hcnt, cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
-  std::vector<uint8_t> rw(end);
-  GRAB_CUDA(cudaMemcpyAsync(rw.data(), rewired, end, cudaMemcpyDeviceToHost, st));
+  {  // rewired slots, ascending, compacted on the device
+    uint32_t* rlist = pool.alloc<uint32_t>(end);
+    uint32_t* nrw_d = pool.alloc<uint32_t>(1);
+    cub::CountingInputIterator<uint32_t> idx(0);
+    size_t tmp = 0;
+    cub::DeviceSelect::If(nullptr, tmp, idx, rlist, nrw_d, (int)end, IsSet{rewired}, st);
+    void* t = pool.alloc<uint8_t>(tmp);
+    GRAB_CUDA(cub::DeviceSelect::If(t, tmp, idx, rlist, nrw_d, (int)end, IsSet{rewired}, st));
+    uint32_t nrw = 0;
+    GRAB_CUDA(cudaMemcpyAsync(&nrw, nrw_d, 4, cudaMemcpyDeviceToHost, st));
+    GRAB_CUDA(cudaStreamSynchronize(st));
+    ix.last_rewired.resize(nrw);
+    if (nrw) GRAB_CUDA(cudaMemcpyAsync(ix.last_rewired.data(), rlist, (size_t)nrw * 4, cudaMemcpyDeviceToHost, st));
+  }
   GRAB_CUDA(cudaStreamSynchronize(st));
-  for (uint64_t s = 0; s < end; ++s)
-    if (rw[s]) ix.last_rewired.push_back((uint32_t)s);
   R.forward_accepted = hcnt.forward_accepted;
   R.forward_rejected = hcnt.forward_rejected;
   R.reverse_accepted = hcnt.reverse_accepted;

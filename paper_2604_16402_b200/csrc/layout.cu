@@ -1,6 +1,7 @@
 // Bucket-slab layout construction, zero-shift appends, slot<->phys translation.
 // Reference behaviour restated: partition map population (layout.py:143-154),
 // append_batch (layout.py:181-223), load_index map rebuild (dataio.py:175-186).
+#include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -51,6 +52,7 @@ static void free_buckets(DevIndex& ix) {
   ix.bound = nullptr;
   ix.bstart = ix.bcount = nullptr;
   ix.bcum = nullptr;
+  ix.m_alloc = 0;
 }
 
 void index_free(DevIndex& ix) {
@@ -92,45 +94,56 @@ static void alloc_phys(DevIndex& ix, uint64_t rows) {
 }
 
 void upload_bucket_tables(DevIndex& ix) {
-  free_buckets(ix);
   uint32_t m = ix.m;
-  GRAB_CUDA(cudaMalloc(&ix.bound, (m + 1) * sizeof(float)));
-  GRAB_CUDA(cudaMalloc(&ix.bstart, std::max(m, 1u) * sizeof(uint32_t)));
-  GRAB_CUDA(cudaMalloc(&ix.bcount, std::max(m, 1u) * sizeof(uint32_t)));
-  GRAB_CUDA(cudaMalloc(&ix.bcum, (m + 1) * sizeof(uint64_t)));
+  // in place when the bucket count is unchanged (every append): stream-ordered
+  // after the writer lock made ix.stream wait for in-flight readers, no
+  // device-wide cudaFree / cudaMalloc synchronisation
+  if (!(ix.bound && ix.bstart && ix.bcount && ix.bcum && ix.m_alloc == m)) {
+    free_buckets(ix);
+    GRAB_CUDA(cudaMalloc(&ix.bound, (m + 1) * sizeof(float)));
+    GRAB_CUDA(cudaMalloc(&ix.bstart, std::max(m, 1u) * sizeof(uint32_t)));
+    GRAB_CUDA(cudaMalloc(&ix.bcount, std::max(m, 1u) * sizeof(uint32_t)));
+    GRAB_CUDA(cudaMalloc(&ix.bcum, (m + 1) * sizeof(uint64_t)));
+    ix.m_alloc = m;
+  }
   std::vector<uint64_t> cum(m + 1, 0);
   for (uint32_t b = 0; b < m; ++b) cum[b + 1] = cum[b] + ix.h_bcount[b];
   GRAB_CUDA(cudaMemcpyAsync(ix.bound, ix.h_bound.data(), (m + 1) * sizeof(float), cudaMemcpyHostToDevice, ix.stream));
   GRAB_CUDA(cudaMemcpyAsync(ix.bstart, ix.h_bstart.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice, ix.stream));
   GRAB_CUDA(cudaMemcpyAsync(ix.bcount, ix.h_bcount.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice, ix.stream));
   GRAB_CUDA(cudaMemcpyAsync(ix.bcum, cum.data(), (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, ix.stream));
-  GRAB_CUDA(cudaStreamSynchronize(ix.stream));  // host vectors may change after return
+  GRAB_CUDA(cudaStreamSynchronize(ix.stream));  // `cum` is a local: the copies must have read it
+}
+
+__global__ void k_iota_u32(uint32_t* out, uint64_t n, uint32_t first) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = first + (uint32_t)i;
 }
 
 // Stable bucket sort of slots [start, start+n): returns device array of slots
-// ordered by (bucket, slot). Caller frees.
+// ordered by (bucket, slot), allocated on ix.stream (caller frees it there).
 static uint32_t* sort_slots_by_bucket(DevIndex& ix, uint64_t start, uint64_t n) {
-  uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
-  GRAB_CUDA(cudaMalloc(&keys_in, n * 4));
-  GRAB_CUDA(cudaMalloc(&keys_out, n * 4));
-  GRAB_CUDA(cudaMalloc(&vals_in, n * 4));
-  GRAB_CUDA(cudaMalloc(&vals_out, n * 4));
-  GRAB_CUDA(cudaMemcpyAsync(keys_in, ix.i2b + start, n * 4, cudaMemcpyDeviceToDevice, ix.stream));
-  std::vector<uint32_t> seq(n);
-  std::iota(seq.begin(), seq.end(), (uint32_t)start);
-  GRAB_CUDA(cudaMemcpyAsync(vals_in, seq.data(), n * 4, cudaMemcpyHostToDevice, ix.stream));
+  cudaStream_t st = ix.stream;
+  uint32_t *keys_out, *vals_in, *vals_out;
+  GRAB_CUDA(cudaMallocAsync(&keys_out, std::max<uint64_t>(n, 1) * 4, st));
+  GRAB_CUDA(cudaMallocAsync(&vals_in, std::max<uint64_t>(n, 1) * 4, st));
+  GRAB_CUDA(cudaMallocAsync(&vals_out, std::max<uint64_t>(n, 1) * 4, st));
+  if (n) {
+    k_iota_u32<<<(unsigned)div_up(n, 256), 256, 0, st>>>(vals_in, n, (uint32_t)start);
+    GRAB_CHECK_LAUNCH();
+  }
   int bits = 1;
   while ((1u << bits) < std::max(ix.m, 2u)) ++bits;
+  // bucket ids are >= 0 here: sorting their low `bits` bits as u32 keys is exact
+  const uint32_t* keys_in = reinterpret_cast<const uint32_t*>(ix.i2b + start);
   size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, bits, ix.stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, bits, st);
   void* tmp;
-  GRAB_CUDA(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
-  GRAB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, bits, ix.stream));
-  GRAB_CUDA(cudaStreamSynchronize(ix.stream));
-  cudaFree(tmp);
-  cudaFree(keys_in);
-  cudaFree(keys_out);
-  cudaFree(vals_in);
+  GRAB_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), st));
+  GRAB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, bits, st));
+  GRAB_CUDA(cudaFreeAsync(tmp, st));
+  GRAB_CUDA(cudaFreeAsync(keys_out, st));
+  GRAB_CUDA(cudaFreeAsync(vals_in, st));
   return vals_out;
 }
 
@@ -155,38 +168,32 @@ __global__ void k_place(const uint32_t* sorted, uint64_t n, const int32_t* i2b, 
   }
 }
 
+// per_bucket: the batch's row count per bucket (from the caller's bucket ids)
 static void place_batch(DevIndex& ix, const float* Xsrc, const float* Ssrc, uint64_t start, uint64_t n,
-                        const std::vector<uint32_t>& base) {
+                        const std::vector<uint32_t>& base, const std::vector<uint32_t>& per_bucket) {
+  cudaStream_t st = ix.stream;
   uint32_t* sorted = sort_slots_by_bucket(ix, start, n);
-  // per-bucket counts within the batch -> first position of each bucket
-  std::vector<int32_t> hb(n);
-  GRAB_CUDA(cudaMemcpyAsync(hb.data(), ix.i2b + start, n * 4, cudaMemcpyDeviceToHost, ix.stream));
-  GRAB_CUDA(cudaStreamSynchronize(ix.stream));
+  // first position of each bucket in the sorted batch
   std::vector<uint64_t> first(ix.m + 1, 0);
-  for (uint64_t i = 0; i < n; ++i) {
-    if (hb[i] < 0 || (uint32_t)hb[i] >= ix.m) throw Error(GRAB_ERR_CUDA, "place: bucket id out of range");
-    first[hb[i] + 1]++;
-  }
-  for (uint32_t b = 0; b < ix.m; ++b) first[b + 1] += first[b];
-  uint32_t* d_base;
-  uint64_t* d_first;
-  GRAB_CUDA(cudaMalloc(&d_base, ix.m * 4));
-  GRAB_CUDA(cudaMalloc(&d_first, (ix.m + 1) * 8));
-  GRAB_CUDA(cudaMemcpyAsync(d_base, base.data(), ix.m * 4, cudaMemcpyHostToDevice, ix.stream));
-  GRAB_CUDA(cudaMemcpyAsync(d_first, first.data(), (ix.m + 1) * 8, cudaMemcpyHostToDevice, ix.stream));
-  uint32_t* d_bstart;
-  GRAB_CUDA(cudaMalloc(&d_bstart, ix.m * 4));
-  GRAB_CUDA(cudaMemcpyAsync(d_bstart, ix.h_bstart.data(), ix.m * 4, cudaMemcpyHostToDevice, ix.stream));
+  for (uint32_t b = 0; b < ix.m; ++b) first[b + 1] = first[b] + per_bucket[b];
+  // one small table upload: base [m] u32 | bstart [m] u32 | first [m+1] u64
+  const size_t tb = (size_t)ix.m * 8 + (size_t)(ix.m + 1) * 8;
+  std::vector<uint8_t> host(tb);
+  std::memcpy(host.data(), base.data(), ix.m * 4);
+  std::memcpy(host.data() + ix.m * 4, ix.h_bstart.data(), ix.m * 4);
+  std::memcpy(host.data() + ix.m * 8, first.data(), (ix.m + 1) * 8);
+  uint8_t* d;
+  GRAB_CUDA(cudaMallocAsync(&d, tb, st));
+  GRAB_CUDA(cudaMemcpyAsync(d, host.data(), tb, cudaMemcpyHostToDevice, st));
   if (n) {
-    k_place<<<(unsigned)n, 32, 0, ix.stream>>>(sorted, n, ix.i2b, d_bstart, d_base, d_first, ix.slot2phys,
-                                               ix.attr, ix.X, ix.dp, Xsrc, Ssrc, ix.dim, start);
+    k_place<<<(unsigned)n, 32, 0, st>>>(sorted, n, ix.i2b, (const uint32_t*)(d + ix.m * 4), (const uint32_t*)d,
+                                        (const uint64_t*)(d + ix.m * 8), ix.slot2phys, ix.attr, ix.X, ix.dp, Xsrc,
+                                        Ssrc, ix.dim, start);
     GRAB_CHECK_LAUNCH();
   }
-  GRAB_CUDA(cudaStreamSynchronize(ix.stream));
-  cudaFree(sorted);
-  cudaFree(d_base);
-  cudaFree(d_first);
-  cudaFree(d_bstart);
+  GRAB_CUDA(cudaFreeAsync(sorted, st));
+  GRAB_CUDA(cudaFreeAsync(d, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));  // `host` is a local: the copy must have read it
 }
 
 void layout_from_slots(DevIndex& ix, const float* X_slot, const float* S_slot, uint64_t count,
@@ -205,7 +212,7 @@ void layout_from_slots(DevIndex& ix, const float* X_slot, const float* S_slot, u
   if (total >= 0xFFFFFFFFull) throw Error(GRAB_ERR_CAPACITY, "physical rows exceed u32 id space");
   alloc_phys(ix, total);
   std::vector<uint32_t> base(ix.m, 0);
-  place_batch(ix, X_slot, S_slot, 0, count, base);
+  place_batch(ix, X_slot, S_slot, 0, count, base, sizes);
   ix.count = count;
   upload_bucket_tables(ix);
 }
@@ -318,7 +325,7 @@ void layout_append(DevIndex& ix, const float* X_new, const float* S_new, uint64_
     if ((uint64_t)ix.h_bcount[k] + extra[k] > ix.h_bcap[k]) overflow = true;
   if (overflow) relayout(ix, extra);
   std::vector<uint32_t> base = ix.h_bcount;
-  place_batch(ix, X_new, S_new, start, b, base);
+  place_batch(ix, X_new, S_new, start, b, base, extra);
   for (uint32_t k = 0; k < ix.m; ++k) ix.h_bcount[k] += extra[k];
   ix.count = start + b;
   upload_bucket_tables(ix);

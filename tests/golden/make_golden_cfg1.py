@@ -1,7 +1,8 @@
 """Freeze BASELINE-shape goldens (configs[0], "cfg1") from the LIVE reference.
 
-Run in the build container (the reference exists only there; ~10 min, most of
-it the reference's own build and its 20K-vector insert):
+Run in the build container (the reference exists only there). The build and
+search goldens (cfg1.npz) take ~3 min; the reference's insert runs at a few
+vectors/s at this size, so the inserts (cfg1_insert.npz) take hours:
 
     PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src \
         python tests/golden/make_golden_cfg1.py
@@ -21,9 +22,11 @@ bucket_capacity 6 250 (m = 16), k = 10. Everything written is an output of
 * the cfg1 workload proper: 1 000 queries at 10 % with default SearchParams and
   the exact filtered brute force (evaluate.py:22-44) -> the reference's
   recall@10 on its own graph;
-* one 20 000-vector ``insert_batch`` (updater.py:154-263) into that graph
-  (``gen_lowrank(20_000, 128, seed=2, w_seed=0)``): the InsertReport counters,
-  the sorted rewired rows and a 64-bit hash of every adjacency row [0, 120K).
+* 20 000 inserted vectors (``gen_lowrank(20_000, 128, seed=2, w_seed=0)``) as
+  four 5 000-vector ``insert_batch`` calls (updater.py:154-263) into that graph,
+  in cfg1_insert.npz: each batch's InsertReport counters and sorted rewired
+  rows, and a 64-bit hash of every adjacency row [0, 100K + inserted) after the
+  last batch done (the file is rewritten per batch; ``ins_batches`` says how many).
 """
 from __future__ import annotations
 
@@ -45,6 +48,7 @@ from make_golden import STAT_KEYS, pack_results  # noqa: E402
 
 N, D, CAP = 100_000, 128, 6_250
 N_INS = 20_000
+INS_BATCHES = 4
 SELS = [0.01, 0.1, 0.5]
 GRID = [dict(k=10, itopk=128, search_width=4, max_iterations=50),
         dict(k=10, itopk=296, search_width=4, max_iterations=100)]
@@ -109,17 +113,24 @@ def main():
     out["w_recall"] = float(np.nanmean(rec))
     print(f"cfg1 workload recall {out['w_recall']:.4f}", flush=True)
 
-    # one 20K insert batch into the reference-built graph
-    Vn, Sn = gen_lowrank(N_INS, D, seed=2, w_seed=0)
-    t0 = time.time()
-    irep = ba.insert_batch(index, Vn, Sn)
-    print(f"insert {time.time() - t0:.1f}s", flush=True)
-    out["ins_report"] = np.array([getattr(irep, k) for k in INSERT_KEYS], np.int64)
-    out["ins_rewired"] = np.array(sorted(irep.rewired_rows), np.uint32)
-    out["ins_row_hash"] = row_hash(index.adjacency[: N + N_INS])
-    out["ins_seconds"] = irep.wall_time_s
     np.savez_compressed(os.path.join(HERE, "cfg1.npz"), **out)
-    print("cfg1.npz", os.path.getsize(os.path.join(HERE, "cfg1.npz")))
+    print("cfg1.npz", os.path.getsize(os.path.join(HERE, "cfg1.npz")), flush=True)
+
+    # 20K inserted rows as INS_BATCHES append-only batches into the reference-built
+    # graph; cfg1_insert.npz is rewritten after every batch (ins_batches = batches done)
+    Vn, Sn = gen_lowrank(N_INS, D, seed=2, w_seed=0)
+    ins = {}
+    per = N_INS // INS_BATCHES
+    for b in range(INS_BATCHES):
+        t0 = time.time()
+        irep = ba.insert_batch(index, Vn[b * per:(b + 1) * per], Sn[b * per:(b + 1) * per])
+        print(f"insert batch {b}: {time.time() - t0:.1f}s", flush=True)
+        ins[f"ins{b}_report"] = np.array([getattr(irep, k) for k in INSERT_KEYS], np.int64)
+        ins[f"ins{b}_rewired"] = np.array(sorted(irep.rewired_rows), np.uint32)
+        ins[f"ins{b}_seconds"] = irep.wall_time_s
+        ins["ins_batches"] = b + 1
+        ins["ins_row_hash"] = row_hash(index.adjacency[: N + (b + 1) * per])
+        np.savez_compressed(os.path.join(HERE, "cfg1_insert.npz"), **ins)
 
 
 if __name__ == "__main__":

@@ -15,10 +15,10 @@ that produce every bench number, on the reference's own graph:
   identical slots and the reference's own recall@10;
 * build (builder.py:503-548): the GPU-built graph's recall@10 within 0.005 of
   the reference-built graph's (north_star), on 10K queries per selectivity;
-* insert (updater.py:154-263): one 20K batch into the reference graph --
-  InsertReport, rewired rows and every adjacency row [0, 120K) as the
-  reference left them; and GPU build + GPU insert vs reference build +
-  insert within 0.005 recall.
+* insert (updater.py:154-263): 20K rows as four 5K batches into the reference
+  graph -- every InsertReport, rewired-row set and adjacency row [0, 120K) as
+  the reference left them (cfg1_insert.npz); and GPU build + GPU insert vs
+  reference build + insert within 0.005 recall.
 """
 import numpy as np
 import pytest
@@ -64,6 +64,9 @@ def data():
 @pytest.fixture(scope="module")
 def gold(golden):
     return golden("cfg1")
+
+
+INS_BATCHES = 4  # make_golden_cfg1.py: 20K inserts as four append-only batches
 
 
 def ref_graph(g, data, gold):
@@ -164,24 +167,31 @@ def test_cfg1_gpu_build_recall_within_tolerance(g, data, gold, gref):
             assert abs(r_gpu - r_ref) <= RECALL_TOL, (sel, p.itopk, r_ref, r_gpu)
 
 
-def test_cfg1_insert_matches_reference(g, data, gold):
-    gi = ref_graph(g, data, gold)
-    rep = g.insert_batch(gi, data["Vn"], data["Sn"])
-    got = [getattr(rep, k) for k in INSERT_KEYS]
-    assert got == gold["ins_report"].tolist()
-    assert np.array_equal(np.array(sorted(rep.rewired_rows), np.uint32), gold["ins_rewired"])
-    h = row_hash(gi.adjacency[: N + N_INS])
+def test_cfg1_insert_matches_reference(g, data, golden):
+    """20K rows inserted as the reference's four 5K batches (as many as the
+    golden holds): every InsertReport, rewired-row set, and adjacency row."""
+    gold = golden("cfg1_insert")
+    nb = int(gold["ins_batches"])
+    per = N_INS // INS_BATCHES
+    gi = ref_graph(g, data, golden("cfg1"))
+    for b in range(nb):
+        rep = g.insert_batch(gi, data["Vn"][b * per:(b + 1) * per], data["Sn"][b * per:(b + 1) * per])
+        assert [getattr(rep, k) for k in INSERT_KEYS] == gold[f"ins{b}_report"].tolist(), b
+        assert np.array_equal(np.array(sorted(rep.rewired_rows), np.uint32), gold[f"ins{b}_rewired"]), b
+    h = row_hash(gi.adjacency[: N + nb * per])
     same = float(np.mean(h == gold["ins_row_hash"]))
-    print(f"cfg1 insert: rows identical to the reference's {same:.6f}")
+    print(f"cfg1 insert ({nb} x {per}): rows identical to the reference's {same:.6f}")
     assert same == 1.0
 
 
 def test_cfg1_gpu_build_and_insert_recall_within_tolerance(g, data, gold):
     from paper_2604_16402_b200.datasets import generate_ranges, range_arrays
+    per = N_INS // INS_BATCHES
     gi_ref = ref_graph(g, data, gold)
-    g.insert_batch(gi_ref, data["Vn"], data["Sn"])  # == the reference's insert (previous test)
     gb, _ = g.build_index(data["X"], data["S"], g.BuildParams(bucket_capacity=CAP))
-    g.insert_batch(gb, data["Vn"], data["Sn"])
+    for b in range(INS_BATCHES):  # on gi_ref: the reference's inserts (previous test, row for row)
+        for gi in (gi_ref, gb):
+            g.insert_batch(gi, data["Vn"][b * per:(b + 1) * per], data["Sn"][b * per:(b + 1) * per])
     S_all = np.concatenate([data["S"], data["Sn"]])
     for sel in SELS:
         lo, hi = range_arrays(generate_ranges(S_all, sel, len(data["Qr"]), 0))

@@ -12,7 +12,14 @@ X, S = ds.gen_lowrank(n, 128, seed=0)
 gi, rep = g.build_index(X, S, g.BuildParams(k_max=32, k_local=16, bucket_capacity=10_000))
 print("build", rep.to_dict() | {"bucket_sizes": None})
 Xi, Si = ds.gen_lowrank(b, 128, seed=2, w_seed=0)
-r = g.insert_batch(gi, Xi, Si)
+import torch  # noqa: E402
+Xd, Sd = torch.from_numpy(Xi).cuda(), torch.from_numpy(Si).cuda()
+g.insert_batch(gi, Xd[:1000], Sd[:1000])  # warm (module load, pools); ncu --profile-from-start off sees the next one
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+r = g.insert_batch(gi, Xd[1000:], Sd[1000:])
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 d = r.to_dict()
 d.pop("rewired_rows")
 print("insert", d)
