@@ -146,8 +146,10 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
   uint32_t* cs = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wib * P;  // slot
   uint32_t* acc_s = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wpb * P +
                     (uint64_t)wib * K;  // accepted slots (K)
+  uint32_t* cph = (uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) + (uint64_t)wpb * (P + K) +
+                  (uint64_t)wib * P;  // phys of each candidate (P): row loads need no slot2phys gather
   uint16_t* alv = (uint16_t*)((uint32_t*)((double*)smem + 2ull * wpb * P + (uint64_t)wpb * K) +
-                              (uint64_t)wpb * (P + K)) + (uint64_t)wib * P;  // live tail indices (P)
+                              (uint64_t)wpb * (2 * P + K)) + (uint64_t)wib * P;  // live tail indices (P)
   const uint64_t q = start + i;
   const uint32_t pq = s2p[q];
   // gather candidates
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
   for (uint32_t j = lane; j < P; j += 32) {
     cd[j] = __longlong_as_double(0x7FF0000000000000ll);
     cs[j] = kSentinel;
+    cph[j] = 0;
   }
   __syncwarp();
   for (uint32_t j = lane; j < KL; j += 32) {
@@ -162,12 +165,15 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
     if (c != kSentinel) {
       cd[j] = loc_d[(uint64_t)pq * KL + j];
       cs[j] = attr[c].slot;
+      cph[j] = c;
     }
   }
   const uint32_t nf = found_cnt ? found_cnt[i] : 0;
   for (uint32_t j = lane; j < nf; j += 32) {
     cd[KL + j] = found_d[i * KS + j];
-    cs[KL + j] = (uint32_t)found_slots[i * KS + j];
+    const uint32_t sj = (uint32_t)found_slots[i * KS + j];
+    cs[KL + j] = sj;
+    cph[KL + j] = s2p[sj];
   }
   __syncwarp();
   // bitonic sort by (dist, slot)
@@ -185,6 +191,9 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
             uint32_t ts = cs[t];
             cs[t] = cs[l];
             cs[l] = ts;
+            ts = cph[t];
+            cph[t] = cph[l];
+            cph[l] = ts;
           }
         }
       }
@@ -204,12 +213,13 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
     bool keep = (keep_bits >> c) & 1u;
     uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
     double dv = cd[t];
-    uint32_t sv = cs[t];
+    uint32_t sv = cs[t], pv = cph[t];
     __syncwarp();
     if (keep) {
       uint32_t pos = n + __popc(m & ((1u << lane) - 1));
       cd[pos] = dv;
       cs[pos] = sv;
+      cph[pos] = pv;
     }
     n += __popc(m);
     __syncwarp();
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
     // is already rejected whatever happens later (nearest_kept only decreases),
     // and self is never accepted, so skipping them changes no decision.
     RowRegs<NC> r;
-    load_row<NC>(r, X, dp, s2p[s]);
+    load_row<NC>(r, X, dp, cph[t]);
     uint32_t na = 0;
     for (uint32_t j0 = t + 1; j0 < n; j0 += 32) {
       const uint32_t j = j0 + lane;
@@ -271,7 +281,7 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           ok[g] = a0 + g < na;
-          p[g] = ok[g] ? s2p[cs[alv[a0 + g]]] : 0u;
+          p[g] = ok[g] ? cph[alv[a0 + g]] : 0u;
         }
         const double dsum = dist_batch<NC>(r, X, dp, p, ok);
         const uint32_t a = a0 + (lane >> SH);
@@ -298,7 +308,7 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
         uint32_t s = acc_s[j];
         bool intra = i2b[s] == bq;
         if ((pass == 0) == intra) {
-          row[col] = s2p[s];
+          row[col] = s2p[s];  // (acc_s holds slots; one gather per accepted edge)
           // reverse request (v, q, d_vq) with the candidate distance
           req_key[i * K + col] = ((unsigned long long)s << 32) | (unsigned long long)q;
           req_d[i * K + col] = acc_d[j];
@@ -803,7 +813,9 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
   for (uint64_t i = 0; i < b; ++i) ix.ids[start + i] = ids ? ids[i] : (int64_t)(start + i);
 
   mark(0);
-  // ---- in-bucket candidates: causal kNN over each touched slab
+  // ---- in-bucket candidates: causal kNN over each touched slab (run beside the
+  // candidate search on a second stream it gains nothing: the search grid holds
+  // every SM and the screen needs a whole SM's shared memory; measured)
   const uint32_t KL = 2 * K;
   uint32_t* loc_ids = pool.alloc<uint32_t>(ix.phys_cap * (uint64_t)KL);
   double* loc_d = pool.alloc<double>(ix.phys_cap * (uint64_t)KL);
@@ -883,7 +895,7 @@ void insert_batch_device(DevIndex& ix, const float* vectors, const float* scalar
   while (P < KL + (n0 > 0 ? KS : 0)) P <<= 1;
   {
     const uint32_t wpb = 4;
-    size_t smem = (size_t)wpb * (P * (8 + 8 + 4 + 2) + K * (8 + 4));
+    size_t smem = (size_t)wpb * (P * (8 + 8 + 4 + 4 + 2) + K * (8 + 4));
     by_nc(ix.dp, [&](auto ncv) {
       constexpr int NC = decltype(ncv)::value;
       auto kern = k_forward<NC>;
