@@ -60,9 +60,9 @@ def row_hash(adj: np.ndarray) -> np.ndarray:
     """Polynomial hash of every u32 row (wrapping u64 arithmetic); tests restate it."""
     p = np.uint64(0x9E3779B97F4A7C15)
     pw = np.ones(adj.shape[1], np.uint64)
-    for j in range(1, adj.shape[1]):
-        pw[j] = pw[j - 1] * p
-    with np.errstate(over="ignore"):
+    with np.errstate(over="ignore"):  # wrapping u64 arithmetic is the point
+        for j in range(1, adj.shape[1]):
+            pw[j] = pw[j - 1] * p
         return (adj.astype(np.uint64) * pw[None, :]).sum(axis=1, dtype=np.uint64)
 
 
