@@ -255,7 +255,27 @@ GRAB_API int grab_shard_pack(uint64_t n, const uint32_t* qidx, const int64_t* sl
 GRAB_API int grab_shard_pack_p2p(uint64_t n, const uint32_t* qidx, const int64_t* slots, const double* dists,
                                  const int64_t* gid, uint32_t k, uint32_t rank, uint32_t world, uint32_t B,
                                  double* const* peer_d, int64_t* const* peer_i, void* stream);
-/* IPC-shareable device buffers: allocate (64-byte handle out), open a peer's, close, free */
+/* The same exchange without any host synchronisation: stream-ordered peer flags.
+ * Each rank owns an IPC-shareable sync block of grab_shard_sync_bytes(world)
+ * bytes, zeroed once (my_sync; peer_sync = device array of every rank's block,
+ * the local one for r == rank), and numbers its batches epoch = 1, 2, ...
+ * identically on every rank. pack_p2p_sync: waits on the device until every
+ * owner has merged batch epoch - 1, writes every entry of this rank's slice of
+ * every owner's buffer (results of the nq-query batch's routed subset, empty
+ * elsewhere), then publishes `epoch` into every owner's ready word for this
+ * rank. merge_topk_p2p: waits on the device until all world ready words reach
+ * `epoch`, merges, then publishes `epoch` into every rank's free word for this
+ * owner. inv_scratch: nq int32 of device scratch. */
+GRAB_API uint64_t grab_shard_sync_bytes(uint32_t world);
+GRAB_API int grab_shard_pack_p2p_sync(uint32_t nq, uint64_t n, const uint32_t* qidx, const int64_t* slots,
+                                      const double* dists, const int64_t* gid, uint32_t k, uint32_t rank,
+                                      uint32_t world, uint32_t B, double* const* peer_d, int64_t* const* peer_i,
+                                      uint64_t* my_sync, uint64_t* const* peer_sync, uint64_t epoch,
+                                      int32_t* inv_scratch, void* stream);
+GRAB_API int grab_merge_topk_p2p(uint32_t nq, uint32_t nsrc, uint32_t B, uint32_t k, const double* d,
+                                 const int64_t* id, double* out_d, int64_t* out_i, uint32_t* out_c, uint32_t rank,
+                                 uint64_t* my_sync, uint64_t* const* peer_sync, uint64_t epoch, void* stream);
+/* IPC-shareable device buffers: allocate (zero-filled, 64-byte handle out), open a peer's, close, free */
 GRAB_API int grab_ipc_alloc(uint64_t bytes, void** ptr, void* handle64);
 GRAB_API int grab_ipc_open(const void* handle64, void** ptr);
 GRAB_API int grab_ipc_close(void* ptr);

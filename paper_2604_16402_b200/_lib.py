@@ -102,6 +102,9 @@ _SIGS = {
     "grab_shard_pack": (C.c_int, [u64, P, P, P, P, u32, u32, u32, P, P, P]),
     "grab_merge_topk": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, P]),
     "grab_shard_pack_p2p": (C.c_int, [u64, P, P, P, P, u32, u32, u32, u32, P, P, P]),
+    "grab_shard_sync_bytes": (u64, [u32]),
+    "grab_shard_pack_p2p_sync": (C.c_int, [u32, u64, P, P, P, P, u32, u32, u32, u32, P, P, P, P, u64, P, P]),
+    "grab_merge_topk_p2p": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, u32, P, P, u64, P]),
     "grab_ipc_alloc": (C.c_int, [u64, C.POINTER(P), P]),
     "grab_ipc_open": (C.c_int, [P, C.POINTER(P)]),
     "grab_ipc_close": (C.c_int, [P]),

@@ -114,13 +114,21 @@ class ShardedIndex:
         import torch.distributed as dist
         if self._peers is not None and self._peers["shape"] == (B, k):
             return self._peers
+        if self._peers is not None and self.world > 1:
+            # (setup, not per batch) every rank is past its last merge before
+            # the old buffers go away
+            torch.cuda.current_stream(self._dev()).synchronize()
+            dist.barrier(group=self.group)
         self.close_peers()
         nbytes = self.world * B * k * 8
         own, handles = [], []
-        for _ in range(2):
+        # receive buffers (dists, ids) and the sync block of the device-side flags
+        # (grab_ipc_alloc zero-fills: the sync block starts at epoch 0 -- every
+        # buffer free, nothing ready)
+        for nb in (nbytes, nbytes, int(L.lib.grab_shard_sync_bytes(self.world))):
             p = C.c_void_p()
             h = (C.c_uint8 * 64)()
-            L.check(L.lib.grab_ipc_alloc(nbytes, C.byref(p), h))
+            L.check(L.lib.grab_ipc_alloc(nb, C.byref(p), h))
             own.append(p.value)
             handles.append(bytes(h))
         if self.world > 1:
@@ -128,9 +136,9 @@ class ShardedIndex:
             dist.all_gather_object(allh, handles, group=self.group)
         else:
             allh = [handles]
-        ptrs, opened = [[0] * self.world, [0] * self.world], []
+        ptrs, opened = [[0] * self.world, [0] * self.world, [0] * self.world], []
         for r in range(self.world):
-            for t in range(2):
+            for t in range(3):
                 if r == self.rank:
                     ptrs[t][r] = own[t]
                 else:
@@ -142,7 +150,11 @@ class ShardedIndex:
         dev = self._dev()
         self._peers = {"shape": (B, k), "own": own, "opened": opened,
                        "ptr_d": torch.tensor(ptrs[0], dtype=torch.int64, device=dev),
-                       "ptr_i": torch.tensor(ptrs[1], dtype=torch.int64, device=dev)}
+                       "ptr_i": torch.tensor(ptrs[1], dtype=torch.int64, device=dev),
+                       "ptr_sync": torch.tensor(ptrs[2], dtype=torch.int64, device=dev), "epoch": 0,
+                       "inv": torch.empty(self.world * B, dtype=torch.int32, device=dev)}
+        if self.world > 1:
+            dist.barrier(group=self.group)  # every rank zeroed its sync block before any pack runs
         return self._peers
 
     def close_peers(self) -> None:
@@ -211,17 +223,16 @@ class ShardedIndex:
         qidx = torch.from_numpy(mine).to(dev)
         stream = torch.cuda.current_stream(dev).cuda_stream
         if self.exchange == "p2p":
-            # fused exchange: stores straight into the owners' receive buffers over NVLink
-            import torch.distributed as dist
+            # fused exchange: stores straight into the owners' receive buffers over
+            # NVLink, ordered by device-side peer flags (epoch per batch): the host
+            # enqueues search -> pack -> merge and never waits
             pb = self._peer_buffers(B, k)
-            if self.world > 1:
-                dist.barrier(group=self.group)  # owners are done merging the previous batch
-            L.check(L.lib.grab_shard_pack_p2p(len(mine), L.ptr(qidx), L.ptr(slots.contiguous()),
-                                              L.ptr(dists.contiguous()), L.ptr(self.gid), k, self.rank, self.world, B,
-                                              L.ptr(pb["ptr_d"]), L.ptr(pb["ptr_i"]), stream))
-            if self.world > 1:
-                torch.cuda.current_stream(dev).synchronize()
-                dist.barrier(group=self.group)  # every rank's stores have landed
+            pb["epoch"] += 1
+            L.check(L.lib.grab_shard_pack_p2p_sync(nq, len(mine), L.ptr(qidx), L.ptr(slots.contiguous()),
+                                                   L.ptr(dists.contiguous()), L.ptr(self.gid), k, self.rank,
+                                                   self.world, B, L.ptr(pb["ptr_d"]), L.ptr(pb["ptr_i"]),
+                                                   C.c_void_p(pb["own"][2]), L.ptr(pb["ptr_sync"]), pb["epoch"],
+                                                   L.ptr(pb["inv"]), stream))
             recv_d, recv_i = C.c_void_p(pb["own"][0]), C.c_void_p(pb["own"][1])
         else:
             send_d = torch.empty((self.world, B, k), dtype=torch.float64, device=dev)
@@ -237,8 +248,13 @@ class ShardedIndex:
         out_c = torch.empty(n_own, dtype=torch.int32, device=dev)
         rd = recv_d if isinstance(recv_d, C.c_void_p) else L.ptr(recv_d)
         ri = recv_i if isinstance(recv_i, C.c_void_p) else L.ptr(recv_i)
-        L.check(L.lib.grab_merge_topk(n_own, self.world, B, k, rd, ri, L.ptr(out_d),
-                                      L.ptr(out_i), L.ptr(out_c), torch.cuda.current_stream(dev).cuda_stream))
+        if self.exchange == "p2p":
+            L.check(L.lib.grab_merge_topk_p2p(n_own, self.world, B, k, rd, ri, L.ptr(out_d), L.ptr(out_i),
+                                              L.ptr(out_c), self.rank, C.c_void_p(pb["own"][2]),
+                                              L.ptr(pb["ptr_sync"]), pb["epoch"], stream))
+        else:
+            L.check(L.lib.grab_merge_topk(n_own, self.world, B, k, rd, ri, L.ptr(out_d),
+                                          L.ptr(out_i), L.ptr(out_c), stream))
         return ShardResult(first, out_i, out_d, out_c, len(mine))
 
 

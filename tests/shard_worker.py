@@ -95,9 +95,27 @@ def run_gpu(rank, world, port, out, exchange="nccl"):
     idx, _ = sh.ShardedIndex.build(X[gid], S[gid], gid, params, rank=rank, world=world, device=0, exchange=exchange)
     sp = g.SearchParams(k=k, itopk=64)
     ex = idx.search(Q, lo, hi, sp, exact=True)
-    se = idx.search(Q, lo, hi, sp, seed_base=0)
-    torch.cuda.synchronize()
     import torch.distributed as dist
+    # count host synchronisation inside the timed-path batch (buffers are set up by
+    # the first batch): the fused p2p exchange must order pack -> merge on the device
+    syncs = {"barrier": 0, "stream_sync": 0, "device_sync": 0}
+    real = (dist.barrier, torch.cuda.Stream.synchronize, torch.cuda.synchronize)
+
+    def _count(key, fn):
+        def w(*a, **kw):
+            syncs[key] += 1
+            return fn(*a, **kw)
+        return w
+    dist.barrier = _count("barrier", real[0])
+    torch.cuda.Stream.synchronize = _count("stream_sync", real[1])
+    torch.cuda.synchronize = _count("device_sync", real[2])
+    try:
+        Qd = torch.from_numpy(Q).cuda()
+        for rep in range(3):  # repeated batches: epochs advance, buffers are reused
+            se = idx.search(Qd, lo, hi, sp, seed_base=0)
+    finally:
+        dist.barrier, torch.cuda.Stream.synchronize, torch.cuda.synchronize = real
+    torch.cuda.synchronize()
     parts = []
     for t in (ex.slots, ex.counts, se.slots, se.counts):
         tc = t.cpu()
@@ -113,7 +131,8 @@ def run_gpu(rank, world, port, out, exchange="nccl"):
         exact_ok = all(parts[0][i, : parts[1][i]].tolist() == ts[i, : tcnt[i]].tolist() for i in range(nq))
         rec = ds.batch_recall(parts[2], parts[3], ts, tcnt, k)
         with open(out, "w") as f:
-            json.dump({"exact_ok": bool(exact_ok), "recall": rec, "routed": int(se.routed)}, f)
+            json.dump({"exact_ok": bool(exact_ok), "recall": rec, "routed": int(se.routed),
+                       "host_syncs_in_search": syncs}, f)
     dist.destroy_process_group()
 
 

@@ -11,7 +11,7 @@ LIB = os.path.join(ROOT, "paper_2604_16402_b200", "libgrab.so")
 
 def declared():
     txt = open(HDR).read()
-    return sorted(set(re.findall(r"GRAB_API\s+(?:int|void|const char\*)\s+(grab_\w+)\s*\(", txt)))
+    return sorted(set(re.findall(r"GRAB_API\s+(?:int|void|uint64_t|const char\*)\s+(grab_\w+)\s*\(", txt)))
 
 
 def test_header_declares_entry_points():

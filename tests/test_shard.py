@@ -92,3 +92,6 @@ def test_sharded_pipeline_p2p_exchange_world2_on_one_gpu(tmp_path):
     res = _run("gpu_p2p", 2, 29545, tmp_path, 600)
     assert res["exact_ok"], res
     assert res["recall"] >= 0.9, res
+    # pack -> merge ordered by device-side peer flags: no barrier, no stream or
+    # device synchronisation on the host during the three search batches
+    assert res["host_syncs_in_search"] == {"barrier": 0, "stream_sync": 0, "device_sync": 0}, res
