@@ -20,6 +20,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -405,6 +407,282 @@ __global__ void __launch_bounds__(32 * WPB) k_descent(const int32_t* joint, cons
   }
 }
 
+// ---------------------------------------------------------------- split round
+// The same round in two phases, so a candidate row is read once per hop SOURCE
+// instead of once per (node, candidate) pair. Node v's hop columns are the
+// joint rows of u = joint[v][hop[h]]; every node that hops through u needs
+// distances to the same J rows joint[u]. So:
+//   A  (k_hop_dists) per source u: its J candidate rows and its users' rows
+//      staged in shared memory, every (user, candidate) distance in f32 by
+//      direct differences -- a screen value within g = dp * 2^-23 (relative)
+//      of the exact squared distance -- written to buf[v][h][j];
+//   B  (k_descent_split) per node: the same first-occurrence flags, then the
+//      k-th smallest screen value T over flagged columns, then the EXACT
+//      distance (group_dist: the direct round's arithmetic, bit for bit) for
+//      every flagged column with screen value <= T (1 + 4 g'), g' >= g, and the
+//      top k of those by (exact, column).
+// Exactness: the k smallest screened columns have exact value <= T(1+g)(1+u),
+// so the exact k-th is below that; a dropped column has exact value >=
+// T(1+4g')(1-g)(1-u) > it, strictly, so it cannot be (or tie) a top-k entry.
+// Own-row columns carry their exact distances already (jd), screen == exact.
+constexpr uint32_t kHopUsers = 16, kHopPad = 132;  // users per chunk; smem row stride (floats)
+
+// sources of every (v, h) pair: key = u (n for a missing column), value = v * nhop + h
+__global__ void k_hop_pairs(const int32_t* joint, uint32_t n, uint32_t J, const uint32_t* hop, uint32_t nhop,
+                            uint32_t* key, uint32_t* val) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= (uint64_t)n * nhop) return;
+  const uint32_t v = (uint32_t)(i / nhop), h = (uint32_t)(i % nhop);
+  const int32_t u = joint[(uint64_t)v * J + hop[h]];
+  key[i] = u >= 0 ? (uint32_t)u : n;
+  val[i] = (uint32_t)i;
+}
+
+__global__ void k_count_src(const uint32_t* key, uint64_t m, uint32_t n, uint32_t* cnt) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < m && key[i] < n) atomicAdd(cnt + key[i], 1u);
+}
+
+// Block per source u (8 warps): warp w takes users 2w, 2w+1 of a 16-user chunk,
+// lane l candidates l and l + 32; 128-float dimension chunks staged with a
+// padded stride (conflict-free float4 reads).
+__global__ void __launch_bounds__(256) k_hop_dists(const uint32_t* off, const uint32_t* sval, uint32_t n,
+                                                   uint32_t nhop, uint32_t J, const int32_t* jointp,
+                                                   const uint32_t* s2p, const float* X, uint32_t dp, float* buf) {
+  __shared__ __align__(16) float cand[64 * kHopPad];
+  __shared__ __align__(16) float usr[kHopUsers * kHopPad];
+  __shared__ int32_t cph[64];
+  __shared__ uint32_t uph[kHopUsers], upair[kHopUsers];
+  const uint32_t u = blockIdx.x;
+  const uint32_t b = off[u], e = off[u + 1];
+  if (b == e) return;  // block-uniform
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (tid < 64) cph[tid] = tid < J ? jointp[(uint64_t)u * J + tid] : -1;
+  const bool one_chunk = dp <= 128;
+  auto load_cand = [&](uint32_t d0) {
+    for (uint32_t i = tid; i < 64 * 32; i += 256) {
+      const uint32_t r = i >> 5, c4 = (i & 31) * 4;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int32_t p = cph[r];
+      if (p >= 0 && d0 + c4 < dp) x = ldg_nc_f4(X + (uint64_t)p * dp + d0 + c4);
+      *reinterpret_cast<float4*>(cand + r * kHopPad + c4) = x;
+    }
+  };
+  __syncthreads();
+  if (one_chunk) load_cand(0);
+  const uint32_t c0 = lane, c1 = lane + 32;
+  for (uint32_t ub = b; ub < e; ub += kHopUsers) {
+    const uint32_t nu = min(kHopUsers, e - ub);
+    __syncthreads();  // the previous chunk's readers are done with usr / uph
+    if (tid < kHopUsers) {
+      const uint32_t pr = tid < nu ? sval[ub + tid] : 0u;
+      upair[tid] = pr;
+      uph[tid] = tid < nu ? s2p[pr / nhop] : 0u;
+    }
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    for (uint32_t d0 = 0; d0 < dp; d0 += 128) {
+      __syncthreads();
+      if (!one_chunk) load_cand(d0);
+      for (uint32_t i = tid; i < kHopUsers * 32; i += 256) {
+        const uint32_t r = i >> 5, c4 = (i & 31) * 4;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < nu && d0 + c4 < dp) x = *reinterpret_cast<const float4*>(X + (uint64_t)uph[r] * dp + d0 + c4);
+        *reinterpret_cast<float4*>(usr + r * kHopPad + c4) = x;
+      }
+      __syncthreads();
+      const uint32_t dl = min(128u, dp - d0);
+      const float* ca = cand + c0 * kHopPad;
+      const float* cb = cand + c1 * kHopPad;
+      const float* ua = usr + (2 * w) * kHopPad;
+      const float* ubr = usr + (2 * w + 1) * kHopPad;
+#pragma unroll 4
+      for (uint32_t f = 0; f < dl; f += 4) {
+        const float4 xa = *reinterpret_cast<const float4*>(ca + f);
+        const float4 xb = *reinterpret_cast<const float4*>(cb + f);
+        const float4 qa = *reinterpret_cast<const float4*>(ua + f);
+        const float4 qb = *reinterpret_cast<const float4*>(ubr + f);
+        const float xv[2][4] = {{xa.x, xa.y, xa.z, xa.w}, {xb.x, xb.y, xb.z, xb.w}};
+        const float qv[2][4] = {{qa.x, qa.y, qa.z, qa.w}, {qb.x, qb.y, qb.z, qb.w}};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const float df = xv[j][t] - qv[i][t];
+              acc[i][j] = fmaf(df, df, acc[i][j]);
+            }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t ui = 2 * w + i;
+      if (ui >= nu) continue;
+      float* row = buf + (uint64_t)upair[ui] * J;  // pair index v * nhop + h
+      const float kInfF = __int_as_float(0x7F800000);
+      if (c0 < J) row[c0] = cph[c0] >= 0 ? acc[i][0] : kInfF;
+      if (c1 < J) row[c1] = cph[c1] >= 0 ? acc[i][1] : kInfF;
+    }
+  }
+}
+
+// Phase B: one warp per node (see the split-round comment above).
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB) k_descent_split(const int32_t* joint, const int32_t* jointp, uint32_t n,
+                                                            uint32_t k, const uint32_t* hop, uint32_t nhop,
+                                                            const uint32_t* s2p, const Attr* attr, const float* X,
+                                                            uint32_t dp, uint32_t C, uint32_t H, int32_t* out_graph,
+                                                            float* out_dist, const float* jd, const float* buf,
+                                                            double gam) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t v = blockIdx.x * WPB + wib;
+  if (v >= n) return;  // warp-uniform
+  const uint32_t NW = (C + 31) / 32;
+  uint8_t* base = smem + (size_t)wib * (C * 4 + NW * 4 + H * 2);
+  int32_t* cid = (int32_t*)base;
+  uint32_t* fl = (uint32_t*)(base + C * 4);
+  unsigned short* hkey = (unsigned short*)(fl + NW);
+  unsigned short* rl = hkey;  // rerank list (columns): the id hash is dead once the flags are set (H >= C)
+  const uint32_t J = 2 * k;
+  const int32_t* jv = joint + (uint64_t)v * J;
+  const uint32_t pv = s2p[v];
+  for (uint32_t i = lane; i < H / 2; i += 32) reinterpret_cast<uint32_t*>(hkey)[i] = 0u;
+  for (uint32_t i = lane; i < J; i += 32) cid[i] = jointp[(uint64_t)v * J + i];
+  for (uint32_t h = 0; h < nhop; ++h) {
+    const int32_t src = jv[hop[h]];
+    for (uint32_t i = lane; i < J; i += 32) cid[J + h * J + i] = src >= 0 ? jointp[(uint64_t)src * J + i] : -1;
+  }
+  __syncwarp();
+  // first occurrence per id, in column order (k_descent's rule)
+  const uint32_t hmask = H - 1;
+  const float kInfF = __int_as_float(0x7F800000);
+  for (uint32_t b0 = 0; b0 < C; b0 += 32) {
+    const uint32_t c = b0 + lane;
+    const int32_t id = c < C ? cid[c] : -1;
+    const uint32_t same = __match_any_sync(0xFFFFFFFFu, (uint32_t)id);
+    const bool lead = id >= 0 && (uint32_t)(__ffs(same) - 1) == lane;
+    uint32_t h = ((uint32_t)id * 0x9E3779B1u) & hmask;
+    const unsigned short me = (unsigned short)(c + 1);
+    uint32_t cur = lead ? atomicCAS(hkey + h, (unsigned short)0, me) : 0u;
+    bool pend = lead && cur != 0u && cid[cur - 1] != id;
+    while (__any_sync(0xFFFFFFFFu, pend)) {
+      if (pend) {
+        h = (h + 1) & hmask;
+        cur = atomicCAS(hkey + h, (unsigned short)0, me);
+        pend = cur != 0u && cid[cur - 1] != id;
+      }
+    }
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, lead && cur == 0u && (uint32_t)id != pv);
+    if (lane == 0) fl[b0 >> 5] = m;
+  }
+  __syncwarp();
+  const float* bv = buf + (uint64_t)v * nhop * J;  // screen values of the hop columns, in column order
+  auto screen = [&](uint32_t c) -> float { return c < J ? jd[(uint64_t)v * J + c] : bv[c - J]; };
+  // running top-k of 32-key chunks (k_descent's bitonic chunk merge)
+  auto merge = [&](uint64_t& best, uint64_t key) {
+    const uint64_t tail = __shfl_sync(0xFFFFFFFFu, best, k - 1);
+    if (!__any_sync(0xFFFFFFFFu, key < tail)) return;
+    for (uint32_t kk = 2; kk <= 32; kk <<= 1)
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, key, j);
+        const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
+        if ((lower == up) ? (o < key) : (o > key)) key = o;
+      }
+    const uint64_t rev = __shfl_sync(0xFFFFFFFFu, key, 31 - lane);
+    best = rev < best ? rev : best;
+    for (uint32_t j = 16; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, best, j);
+      const bool lower = (lane & j) == 0;
+      if (lower ? (o < best) : (o > best)) best = o;
+    }
+  };
+  // (1) the k-th smallest screen value over the flagged columns
+  uint64_t sbest = ~0ull;
+  for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+    const uint32_t c = c0 + lane;
+    const bool f = c < C && ((fl[c0 >> 5] >> lane) & 1u);
+    merge(sbest, f ? dc_key(screen(c), c) : ~0ull);
+  }
+  const uint64_t tk = __shfl_sync(0xFFFFFFFFu, sbest, k - 1);
+  const double bound = tk == ~0ull ? __longlong_as_double(0x7FF0000000000000ll)
+                                   : (double)__uint_as_float((uint32_t)(tk >> 32)) * (1.0 + 4.0 * gam);
+  // (2) columns that can still be in the top k, in column order
+  uint32_t nr = 0;
+  for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+    const uint32_t c = c0 + lane;
+    const bool take = c < C && ((fl[c0 >> 5] >> lane) & 1u) && (double)screen(c) <= bound;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, take);
+    if (take) rl[nr + __popc(m & ((1u << lane) - 1))] = (unsigned short)c;
+    nr += __popc(m);
+  }
+  __syncwarp();
+  // (3) exact distances of those (own columns: jd; hop columns: group_dist in
+  // k_descent's lane groups) and the top k by (exact, column)
+  const float* qrow = X + (uint64_t)pv * dp;
+  const uint32_t sub = lane & 7, grp = lane >> 3;
+  uint64_t best = ~0ull;
+  for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
+    double sums[8];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t pc[4];
+      bool ok[4];
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+        const uint32_t idx = r0 + grp * 8 + half * 4 + uu;
+        const uint32_t c = idx < nr ? rl[idx] : 0u;
+        ok[uu] = idx < nr && c >= J;
+        pc[uu] = ok[uu] ? (uint32_t)cid[c] : 0u;
+      }
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (__any_sync(0xFFFFFFFFu, ok[0] | ok[1] | ok[2] | ok[3])) {
+#pragma unroll 2
+        for (uint32_t f = sub; f * 4 < dp; f += 8) {
+          const float4 q = *reinterpret_cast<const float4*>(qrow + 4 * f);
+          float4 x[4];
+#pragma unroll
+          for (int uu = 0; uu < 4; ++uu) x[uu] = ok[uu] ? ldg_nc_f4(X + (uint64_t)pc[uu] * dp + 4 * f) : q;
+#pragma unroll
+          for (int uu = 0; uu < 4; ++uu) acc[uu] = sq4(x[uu], q, acc[uu]);
+        }
+      }
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+        acc[uu] += __shfl_xor_sync(0xFFFFFFFFu, acc[uu], 4);
+        acc[uu] += __shfl_xor_sync(0xFFFFFFFFu, acc[uu], 2);
+        acc[uu] += __shfl_xor_sync(0xFFFFFFFFu, acc[uu], 1);
+        sums[half * 4 + uu] = acc[uu];
+      }
+    }
+    double mine = sums[0];
+#pragma unroll
+    for (int uu = 1; uu < 8; ++uu) mine = sub == (uint32_t)uu ? sums[uu] : mine;
+    const uint32_t idx = r0 + lane;
+    uint64_t key = ~0ull;
+    if (idx < nr) {
+      const uint32_t c = rl[idx];
+      key = dc_key(c < J ? jd[(uint64_t)v * J + c] : (float)mine, c);
+    }
+    merge(best, key);
+  }
+  if (nr < k) {
+    // fewer than k flagged columns: like k_descent, the rest of the row is the
+    // (inf, column) keys of the unflagged columns, lowest columns first
+    for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+      const uint32_t c = c0 + lane;
+      const bool uf = c < C && !((fl[c0 >> 5] >> lane) & 1u);
+      merge(best, uf ? dc_key(kInfF, c) : ~0ull);
+    }
+  }
+  if (lane < k) {
+    const uint32_t col = (uint32_t)best;
+    const int32_t pid = best == ~0ull ? -1 : cid[col];
+    out_graph[(uint64_t)v * k + lane] = pid >= 0 ? (int32_t)attr[pid].slot : -1;
+    out_dist[(uint64_t)v * k + lane] = __uint_as_float((uint32_t)(best >> 32));
+  }
+}
+
 // descent rows (slot ids) -> pass-2 forward rows in phys space with f64
 // distances (the exact path's contract for the reverse merge)
 __global__ void k_descent_to_phys(const int32_t* graph, uint32_t n, uint32_t k, const float* dist,
@@ -525,6 +803,30 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
   constexpr int WPB = 1;
   const size_t smem = (size_t)WPB * (C * 4 + (C + 31) / 32 * 4 + H * 2);
   GRAB_CUDA(cudaFuncSetAttribute(k_descent<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // split rounds (screen per hop source + exact rerank) while the per-node screen
+  // buffer stays within budget; the direct kernel otherwise (and on request)
+  const uint64_t npairs = (uint64_t)n * nhop;
+  const bool split = !getenv("GRAB_DESCENT_DIRECT") && J <= 64 && npairs * J * 4 <= (12ull << 30) &&
+                     npairs < 0xFFFFFFFFull;
+  float* sbuf = nullptr;
+  uint32_t *pkey = nullptr, *pval = nullptr, *pkeys = nullptr, *pvals = nullptr, *scnt = nullptr, *soff = nullptr;
+  void* ptmp = nullptr;
+  size_t ptmp_bytes = 0;
+  const size_t smem_s = smem;  // (the rerank list aliases the id hash)
+  // screen error bound: direct f32 differences, dp products summed in order
+  const double gam = std::max(std::ldexp(1.0, -14), (double)ix.dp * std::ldexp(1.0, -22));
+  if (split) {
+    sbuf = S.alloc<float>(npairs * J);
+    pkey = S.alloc<uint32_t>(npairs);
+    pval = S.alloc<uint32_t>(npairs);
+    pkeys = S.alloc<uint32_t>(npairs);
+    pvals = S.alloc<uint32_t>(npairs);
+    scnt = S.alloc<uint32_t>(n + 1);
+    soff = S.alloc<uint32_t>(n + 1);
+    cub::DeviceRadixSort::SortPairs(nullptr, ptmp_bytes, pkey, pkeys, pval, pvals, (int)npairs, 0, end_bit, st);
+    ptmp = S.alloc<uint8_t>(ptmp_bytes);
+    GRAB_CUDA(cudaFuncSetAttribute(k_descent_split<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+  }
   for (uint32_t r = 0; r < rounds; ++r) {
     // reverse top-k: stable sort by (dist, src), then by dst
     k_rev_keys<<<(unsigned)div_up(nk, 256), 256, 0, st>>>(graph, dist, nk, k, n, key2, dst);
@@ -548,10 +850,26 @@ void descent_device(const DevIndex& ix, uint64_t n64, uint32_t k, uint32_t round
     GRAB_CUDA(cudaMemcpyAsync(dhop, perm.data(), nhop * 4, cudaMemcpyHostToDevice, st));
     k_joint_phys<<<(unsigned)div_up((uint64_t)n * J, 256), 256, 0, st>>>(joint, (uint64_t)n * J, ix.slot2phys, jointp);
     GRAB_CHECK_LAUNCH();
-    k_descent<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem, st>>>(joint, jointp, n, k, dhop, nhop, ix.slot2phys,
-                                                                     ix.attr, ix.X,
-                                                                     ix.dp, C, H, g2, d2, jd);
-    GRAB_CHECK_LAUNCH();
+    if (split) {
+      // users of every hop source (CSR by source), their screen distances, then the nodes
+      k_hop_pairs<<<(unsigned)div_up(npairs, 256), 256, 0, st>>>(joint, n, J, dhop, nhop, pkey, pval);
+      GRAB_CHECK_LAUNCH();
+      GRAB_CUDA(cub::DeviceRadixSort::SortPairs(ptmp, ptmp_bytes, pkey, pkeys, pval, pvals, (int)npairs, 0, end_bit,
+                                                st));
+      GRAB_CUDA(cudaMemsetAsync(scnt, 0, (n + 1) * 4, st));
+      k_count_src<<<(unsigned)div_up(npairs, 256), 256, 0, st>>>(pkeys, npairs, n, scnt);
+      GRAB_CHECK_LAUNCH();
+      exclusive_scan_u32(scnt, soff, n + 1, st);
+      k_hop_dists<<<n, 256, 0, st>>>(soff, pvals, n, nhop, J, jointp, ix.slot2phys, ix.X, ix.dp, sbuf);
+      GRAB_CHECK_LAUNCH();
+      k_descent_split<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem_s, st>>>(
+          joint, jointp, n, k, dhop, nhop, ix.slot2phys, ix.attr, ix.X, ix.dp, C, H, g2, d2, jd, sbuf, gam);
+      GRAB_CHECK_LAUNCH();
+    } else {
+      k_descent<WPB><<<(unsigned)div_up(n, WPB), 32 * WPB, smem, st>>>(joint, jointp, n, k, dhop, nhop, ix.slot2phys,
+                                                                       ix.attr, ix.X, ix.dp, C, H, g2, d2, jd);
+      GRAB_CHECK_LAUNCH();
+    }
     std::swap(graph, g2);
     std::swap(dist, d2);
     GRAB_CUDA(cudaStreamSynchronize(st));  // `perm` and the scratch stay valid across the round

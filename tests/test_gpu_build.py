@@ -177,3 +177,26 @@ def test_partition_buckets_matches_reference_goldens(g, golden):
         assert all(meta.index_to_bucket[x] == bi for bi, b in enumerate(meta.bucket_to_index) for x in b)
     with pytest.raises(ValueError):
         g.partition_buckets(np.zeros(0, np.float32), 10)
+
+
+@pytest.mark.parametrize("n,d,kg,rounds", [(30_000, 32, 32, 3), (12_000, 200, 16, 2), (5_000, 8, 8, 1)])
+def test_split_descent_rounds_equal_direct_rounds(g, n, d, kg, rounds):
+    """descent.cu's split round (per-hop-source f32 screen, exact rerank of the
+    columns that can still be in the top k) returns the direct round's rows
+    bit for bit: same global rows, same final adjacency."""
+    import os
+    from paper_2604_16402_b200.datasets import gen_lowrank
+    X, S = gen_lowrank(n, d, seed=11)
+    params = g.BuildParams(k_max=32, k_local=16, bucket_capacity=max(1000, n // 10))
+    out = {}
+    for mode in ("direct", "split"):
+        if mode == "direct":
+            os.environ["GRAB_DESCENT_DIRECT"] = "1"
+        try:
+            gi, rep, dr = g.build_index(X, S, params, k_g=kg, refine_rounds=rounds, return_draft=True,
+                                        global_pass="descent")
+        finally:
+            os.environ.pop("GRAB_DESCENT_DIRECT", None)
+        out[mode] = (dr.global_rows.copy(), gi.adjacency[:n].copy())
+    assert np.array_equal(out["split"][0], out["direct"][0])
+    assert np.array_equal(out["split"][1], out["direct"][1])
