@@ -597,22 +597,45 @@ __global__ void __launch_bounds__(32 * WPB) k_descent_split(const int32_t* joint
       if (lower ? (o < best) : (o > best)) best = o;
     }
   };
-  // (1) the k-th smallest screen value over the flagged columns
-  uint64_t sbest = ~0ull;
+  // (1) the k-th smallest screen value T over the flagged columns. The own
+  // row's flagged columns are exact and contain at least k of them in the
+  // common case, so their k-th smallest value Tu >= T bounds every column
+  // that matters: only columns with screen value <= Tu (1 + 4g) are collected
+  // (into rl) and ranked, instead of every one of the C columns.
+  uint64_t obest = ~0ull;
+  for (uint32_t c0 = 0; c0 < J; c0 += 32) {
+    const uint32_t c = c0 + lane;
+    const bool f = c < J && ((fl[c0 >> 5] >> lane) & 1u);
+    merge(obest, f ? dc_key(jd[(uint64_t)v * J + c], c) : ~0ull);
+  }
+  const uint64_t tu = __shfl_sync(0xFFFFFFFFu, obest, k - 1);
+  const double kInfD = __longlong_as_double(0x7FF0000000000000ll);
+  const double ubound = tu == ~0ull ? kInfD : (double)__uint_as_float((uint32_t)(tu >> 32)) * (1.0 + 4.0 * gam);
+  uint32_t nl = 0;
   for (uint32_t c0 = 0; c0 < C; c0 += 32) {
     const uint32_t c = c0 + lane;
-    const bool f = c < C && ((fl[c0 >> 5] >> lane) & 1u);
-    merge(sbest, f ? dc_key(screen(c), c) : ~0ull);
+    const bool take = c < C && ((fl[c0 >> 5] >> lane) & 1u) && (double)screen(c) <= ubound;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, take);
+    if (take) rl[nl + __popc(m & ((1u << lane) - 1))] = (unsigned short)c;
+    nl += __popc(m);
+  }
+  __syncwarp();
+  uint64_t sbest = ~0ull;
+  for (uint32_t i0 = 0; i0 < nl; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t c = i < nl ? rl[i] : 0u;
+    merge(sbest, i < nl ? dc_key(screen(c), c) : ~0ull);
   }
   const uint64_t tk = __shfl_sync(0xFFFFFFFFu, sbest, k - 1);
-  const double bound = tk == ~0ull ? __longlong_as_double(0x7FF0000000000000ll)
-                                   : (double)__uint_as_float((uint32_t)(tk >> 32)) * (1.0 + 4.0 * gam);
-  // (2) columns that can still be in the top k, in column order
+  const double bound = tk == ~0ull ? kInfD : (double)__uint_as_float((uint32_t)(tk >> 32)) * (1.0 + 4.0 * gam);
+  // (2) columns that can still be in the top k (a subset of rl, kept in order)
   uint32_t nr = 0;
-  for (uint32_t c0 = 0; c0 < C; c0 += 32) {
-    const uint32_t c = c0 + lane;
-    const bool take = c < C && ((fl[c0 >> 5] >> lane) & 1u) && (double)screen(c) <= bound;
+  for (uint32_t i0 = 0; i0 < nl; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t c = i < nl ? rl[i] : 0u;
+    const bool take = i < nl && (double)screen(c) <= bound;
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, take);
+    __syncwarp();  // the chunk is read before the compaction writes into it
     if (take) rl[nr + __popc(m & ((1u << lane) - 1))] = (unsigned short)c;
     nr += __popc(m);
   }
