@@ -391,11 +391,13 @@ def _timed(fn, stream):
     return e0.elapsed_time(e1), out
 
 
-def _warm_build(g, ds, dim, params, device, global_pass):
-    """One untimed 120K-row build with the same kernels (pass 1, NN-descent above
-    100K rows, fuse): loads the lazily-loaded CUDA modules and grows the
-    stream-ordered memory pool, so build_s is the steady-state build time."""
-    Xw, Sw = ds.gen_lowrank(120_000, dim, seed=7)
+def _warm_build(g, ds, dim, params, device, global_pass, n=120_000):
+    """One untimed build with the same kernels (pass 1, NN-descent above 100K
+    rows, fuse) on other data of the timed size: loads the lazily-loaded CUDA
+    modules and grows the stream-ordered memory pool to the build's peak
+    scratch (the split descent's screen buffer is ~4 GB at 1M rows), so build_s
+    is the steady-state build time of a process that has built before."""
+    Xw, Sw = ds.gen_lowrank(max(n, 120_000), dim, seed=7)
     gw, _ = g.build_index(Xw, Sw, params, device=device, global_pass=global_pass)
     del gw
 
@@ -700,7 +702,7 @@ def main():
     # build_s = median of 3 builds of the same inputs (deterministic: identical
     # graphs), after one untimed small warm-up build; the first build of the
     # process is reported separately (module load, pool growth, first touch)
-    _warm_build(g, ds, dim, params, local, args.global_pass)
+    _warm_build(g, ds, dim, params, local, args.global_pass, n=n)
     build_times = []
     for b in range(3):
         gi = None
@@ -758,7 +760,7 @@ def main():
               "index": "replicated per GPU" if world > 1 else "single GPU",
               "global_pass": brep.global_pass,
               "build_timing": "median of 3 build_index calls (host arrays in, upload included; host wall "
-                              "clock) after one untimed 120K-row warm-up build"}
+                              "clock) after one untimed warm-up build of the same size on other data"}
 
     if args.export_graph:
         # fixture for the reference arm (a separate process that never loads libgrab):
