@@ -576,6 +576,22 @@ __device__ uint32_t sample_seeds(const SearchArgs& a, uint32_t* stage, uint32_t*
   return picked;
 }
 
+// ---------------------------------------------------------------- phase profile
+// -DGRAB_SEARCH_PROFILE: per-phase SM cycles summed over all warps (lab only;
+// run_search prints the split after each launch). Phases: 0 query setup +
+// seeds, 1 frontier, 2 adjacency gather + pre-check, 3 visited set,
+// 4 compaction, 5 distances, 6 admit.
+#ifdef GRAB_SEARCH_PROFILE
+__device__ unsigned long long g_phase[8];
+#define PROF_INIT() long long prof_t = clock64(); unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define PROF(i) { const long long t_ = clock64(); prof_acc[i] += (unsigned long long)(t_ - prof_t); prof_t = t_; }
+#define PROF_FLUSH() if (lane == 0) { for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_phase[i_], prof_acc[i_]); }
+#else
+#define PROF_INIT()
+#define PROF(i)
+#define PROF_FLUSH()
+#endif
+
 // ---------------------------------------------------------------- kernel
 // NC: 128-float chunks per row; EPL: gathered neighbours per lane per iteration
 // (width * K_max <= 32 * EPL).
@@ -615,6 +631,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
     if (lane == 0) it = atomicAdd(a.work_ctr, 1u);
     return __shfl_sync(kFull, it, 0);
   };
+  PROF_INIT()
   for (uint32_t item = a.work_ctr ? next_item(0) : gw; item < nwork; item = next_item(item)) {
     const uint32_t qi = a.qmap ? a.qmap[item] : item;
     const float lo_f = __double2float_rn(a.lower[(uint64_t)qi * a.range_stride]);
@@ -651,6 +668,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
         score<NC, FULL>(qr, a.X, a.dp, cp, cd, ns);
         dist_evals = seed_evals = ns;
         L = admit(qe, cd, cs, cp, 0, ns, sh.itopk, fu);
+        PROF(0)
         for (uint32_t it = 0; it < a.max_iter; ++it) {
           // frontier: first `width` unexpanded entries (searcher.py:73-79)
           uint32_t nf = 0;
@@ -674,6 +692,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
             nf += __popc(pm);
           }
           __syncwarp();
+          PROF(1)
           if (nf == 0) break;
           const uint32_t fan = nf * K;
           if (!vis.bm && vis_n + fan > vcap) {  // (a bitmap cannot overflow)
@@ -709,6 +728,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
             const float sv = __uint_as_float(at[t].x);
             cand_bits |= (at[t].y < a.n_live && sv >= lo_f && sv <= hi_f) ? 1u << t : 0u;
           }
+          PROF(2)
           // every first-probe CAS in flight before any is consumed; the table
           // (load <= 1/4) is left all-zero again by undoing this iteration's inserts
           auto count_unique = [&]() {
@@ -785,6 +805,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
             }
           }
           __syncwarp();
+          PROF(3)
           // (4) compact candidates in gather order
           uint32_t nc = 0;
 #pragma unroll
@@ -800,11 +821,14 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
           }
           __syncwarp();
           vis_n += nc;
+          PROF(4)
           if (nc == 0) continue;
           dist_evals += nc;
           pad_cands(cp, nc);
           score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc);
+          PROF(5)
           L = admit(qe, cd, cs, cp, L, nc, sh.itopk, fu);
+          PROF(6)
         }
       }
     }
@@ -851,7 +875,9 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
       }
     }
     __syncwarp();
+    PROF(7)
   }
+  PROF_FLUSH()
 }
 
 // adja[i] = attr[adj[i]] ({NaN, kNoSlot} for SENTINEL)
@@ -993,8 +1019,9 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
       occ[key] = per_sm;
     }
   }
-  const uint64_t blocks =
-      std::min<uint64_t>(std::min<uint64_t>(div_up(a.nwork, wpb), (uint64_t)per_sm * num_sms), max_blocks);
+  uint64_t cap_blocks = (uint64_t)per_sm * num_sms;
+  if (const char* e = getenv("GRAB_SEARCH_BLOCKS")) cap_blocks = std::min<uint64_t>(cap_blocks, strtoull(e, 0, 10));
+  const uint64_t blocks = std::min<uint64_t>(std::min<uint64_t>(div_up(a.nwork, wpb), cap_blocks), max_blocks);
   if (!blocks) return;
   // one visited table per resident warp
   const uint64_t words = blocks * wpb * (1ull << sh.vlog2);
@@ -1089,7 +1116,25 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.ovf_list = ovf + 1;
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
+#ifdef GRAB_SEARCH_PROFILE
+  {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    GRAB_CUDA(cudaMemcpyToSymbolAsync(g_phase, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+  }
+#endif
   launch(a, sh, ix.num_sms, st, tables, ~0ull);
+#ifdef GRAB_SEARCH_PROFILE
+  {
+    unsigned long long z[8];
+    GRAB_CUDA(cudaMemcpyFromSymbolAsync(z, g_phase, sizeof(z), 0, cudaMemcpyDeviceToHost, st));
+    GRAB_CUDA(cudaStreamSynchronize(st));
+    double tot = 0;
+    for (int i = 0; i < 8; ++i) tot += (double)z[i];
+    fprintf(stderr, "[grab] search phases %%: setup+seeds %.1f frontier %.1f gather %.1f visited %.1f compact %.1f "
+                    "score %.1f admit %.1f output %.1f\n", 100 * z[0] / tot, 100 * z[1] / tot, 100 * z[2] / tot,
+            100 * z[3] / tot, 100 * z[4] / tot, 100 * z[5] / tot, 100 * z[6] / tot, 100 * z[7] / tot);
+  }
+#endif
   SearchShape big = make_shape(a.itopk, a.width, a.k_max, a.want, a.max_iter, true, a.dp, a.n_live,
                                a.out_stats != nullptr);
   // the retry grid's tables: at most ~1 GB (fewer resident warps for huge tables;
