@@ -52,7 +52,7 @@ struct SearchShape {
 };
 
 SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t want, uint32_t max_iter, bool worst,
-                       uint32_t dp, uint64_t live_rows, bool stats);
+                       uint32_t dp, uint64_t live_rows, bool stats, uint64_t phys_rows);
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st);
 
 }  // namespace grab
