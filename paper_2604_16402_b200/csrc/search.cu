@@ -63,40 +63,57 @@ __device__ __forceinline__ uint32_t hash32(uint32_t k) { return k * 0x9E3779B1u;
 // policy so the ~45 MB of live tables stay resident under the row stream
 // (-DGRAB_VIS_NO_HINT restores plain accesses for A/B).
 #ifndef GRAB_VIS_NO_HINT
-__device__ __forceinline__ uint64_t vis_policy() {
+// L2 policy of one query's table: evict_last for tables small enough that every
+// resident warp's table fits the persisting set-aside (narrow ranges: 1 % and
+// 10 % at 1M rows), evict_normal for wide ones (50 %: 222 MB of tables would
+// only crowd the candidate rows out of L2)
+__device__ __forceinline__ uint64_t vis_make_policy(bool persist) {
   uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  if (persist)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ uint32_t vis_or(uint32_t* a, uint32_t v) {
+__device__ __forceinline__ uint32_t vis_or(uint32_t* a, uint32_t v, uint64_t pol) {
   uint32_t o;
-  asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
-               : "=r"(o) : "l"(a), "r"(v), "l"(vis_policy()) : "memory");
+  asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(a), "r"(v), "l"(pol) : "memory");
   return o;
 }
 // (ptxas rejects .L2::cache_hint on atom.cas: the hash mode's CAS is plain; its
 // lines are kept hot by the hinted loads that probe them)
 __device__ __forceinline__ uint32_t vis_cas(uint32_t* a, uint32_t cmp, uint32_t v) { return atomicCAS(a, cmp, v); }
-__device__ __forceinline__ uint32_t vis_ld(const uint32_t* a) {
+__device__ __forceinline__ uint32_t vis_ld(const uint32_t* a, uint64_t pol) {
   uint32_t o;  // .cg: the L2 copy (the atomics live there), never a stale L1 line
-  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(o) : "l"(a), "l"(vis_policy()) : "memory");
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(o) : "l"(a), "l"(pol) : "memory");
   return o;
 }
-__device__ __forceinline__ void vis_clear(uint32_t* p, uint32_t n) {
-  const uint64_t pol = vis_policy();
+__device__ __forceinline__ void vis_clear(uint32_t* p, uint32_t n, uint64_t pol) {
   for (uint32_t i = lane_id() * 4; i < n; i += 128)
     asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(p + i), "r"(0u), "l"(pol)
                  : "memory");
 }
 #else
-__device__ __forceinline__ uint32_t vis_or(uint32_t* a, uint32_t v) { return atomicOr(a, v); }
+__device__ __forceinline__ uint64_t vis_make_policy(bool) { return 0; }
+__device__ __forceinline__ uint32_t vis_or(uint32_t* a, uint32_t v, uint64_t) { return atomicOr(a, v); }
 __device__ __forceinline__ uint32_t vis_cas(uint32_t* a, uint32_t cmp, uint32_t v) { return atomicCAS(a, cmp, v); }
-__device__ __forceinline__ uint32_t vis_ld(const uint32_t* a) { return *((volatile const uint32_t*)a); }
-__device__ __forceinline__ void vis_clear(uint32_t* p, uint32_t n) {
+__device__ __forceinline__ uint32_t vis_ld(const uint32_t* a, uint64_t) { return *((volatile const uint32_t*)a); }
+__device__ __forceinline__ void vis_clear(uint32_t* p, uint32_t n, uint64_t) {
   const uint4 z = make_uint4(0, 0, 0, 0);
   for (uint32_t i = lane_id() * 4; i < n; i += 128) *reinterpret_cast<uint4*>(p + i) = z;
 }
 #endif
+#ifndef GRAB_VIS_PERSIST_BYTES
+#define GRAB_VIS_PERSIST_BYTES 16384u
+#endif
+// At query end a persisting table is dead (the next query clears it first):
+// drop its lines from L2 without write-back, so persisting lines never linger
+// into later launches (left in the set-aside they cost wide ranges a third of
+// the L2 for normal lines: 20 % selectivity 5.8 -> 8.0 ms, measured).
+__device__ __forceinline__ void vis_release(uint32_t* p, uint32_t n) {
+  for (uint32_t i = lane_id() * 32; i < n; i += 32 * 32)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p + i) : "memory");
+}
 
 // Open-addressing set of 2^lg u32 entries (value key+1, 0 = empty).
 // Every probe loop is warp-uniform (all 32 lanes iterate until no lane has a
@@ -121,16 +138,17 @@ __device__ __forceinline__ bool set_insert_w(uint32_t* tab, uint32_t lg, uint32_
 }
 
 // True for active lanes whose key is present.
-__device__ __forceinline__ bool set_contains_w(const uint32_t* tab, uint32_t lg, uint32_t key, bool active) {
+__device__ __forceinline__ bool set_contains_w(const uint32_t* tab, uint32_t lg, uint32_t key, bool active,
+                                               uint64_t pol) {
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = hash32(key) >> (32 - lg);
   const uint32_t v = key + 1;
-  uint32_t cur = active ? vis_ld(tab + h) : 0u;
+  uint32_t cur = active ? vis_ld(tab + h, pol) : 0u;
   bool pending = active && cur != 0u && cur != v;
   while (__any_sync(0xFFFFFFFFu, pending)) {
     if (pending) {
       h = (h + 1) & mask;
-      cur = vis_ld(tab + h);
+      cur = vis_ld(tab + h, pol);
       pending = cur != 0u && cur != v;
     }
   }
@@ -148,20 +166,21 @@ struct Visited {
   uint32_t* tab;
   uint32_t lg, base, nbits;
   bool bm;
+  uint64_t pol;  // L2 policy of this query's table accesses
   __device__ __forceinline__ uint32_t clear_words_n() const {
     return bm ? ((nbits + 4095u) >> 12) << 7 : (1u << lg);  // multiple of 128 words
   }
   __device__ __forceinline__ bool contains_w(uint32_t key, bool active) const {
     if (bm) {
       const uint32_t o = key - base;
-      return active && (vis_ld(tab + (o >> 5)) >> (o & 31) & 1u);
+      return active && (vis_ld(tab + (o >> 5), pol) >> (o & 31) & 1u);
     }
-    return set_contains_w(tab, lg, key, active);
+    return set_contains_w(tab, lg, key, active, pol);
   }
   __device__ __forceinline__ bool insert_w(uint32_t key, bool active) const {
     if (bm) {
       const uint32_t o = key - base;
-      return active && !(vis_or(tab + (o >> 5), 1u << (o & 31)) >> (o & 31) & 1u);
+      return active && !(vis_or(tab + (o >> 5), 1u << (o & 31), pol) >> (o & 31) & 1u);
     }
     return set_insert_w(tab, lg, key, active);
   }
@@ -654,7 +673,9 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
       vis.base = __ldg(a.bstart + lo_b);
       vis.nbits = __ldg(a.bstart + hi_b) + __ldg(a.bcount + hi_b) - vis.base;
       vis.bm = vis.nbits <= (32u << vlg);
-      vis_clear(vtab, vis.clear_words_n());
+      vis.pol = vis_make_policy(vis.clear_words_n() * 4u <= GRAB_VIS_PERSIST_BYTES);
+      vis_clear(vtab, vis.clear_words_n(), vis.pol);
+      if (lane == 0 && a.tab_words) atomicAdd(a.tab_words, (unsigned long long)vis.clear_words_n());
       __syncwarp();
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
       const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
@@ -770,7 +791,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
 #pragma unroll
               for (int t = 0; t < EPL; ++t) {
                 const uint32_t o = v[t] - vis.base;
-                cur[t] = ((cand_bits >> t) & 1u) ? vis_or(vtab + (o >> 5), 1u << (o & 31)) : 0u;
+                cur[t] = ((cand_bits >> t) & 1u) ? vis_or(vtab + (o >> 5), 1u << (o & 31), vis.pol) : 0u;
               }
               if constexpr (STATS) count_unique();  // overlaps the visited atomics' round trip
 #pragma unroll
@@ -830,6 +851,10 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
           L = admit(qe, cd, cs, cp, L, nc, sh.itopk, fu);
           PROF(6)
         }
+      }
+      if (vis.clear_words_n() * 4u <= GRAB_VIS_PERSIST_BYTES) {
+        __syncwarp();  // every lane's table accesses are done
+        vis_release(vtab, vis.clear_words_n());
       }
     }
     if (overflow) {
@@ -1050,7 +1075,16 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
 // order makes the reuse safe without host synchronization).
 struct SearchWs {
   std::mutex mu;  // host-side: one enqueue at a time per stream (threads may share a stream)
-  DBufLite tables, big_tables, ovf, ctr;
+  DBufLite tables, big_tables, ovf, ctr, tabw;
+  // the previous launch's visited-table footprint, copied back asynchronously
+  unsigned long long* tabw_host = nullptr;  // pinned
+  cudaEvent_t tabw_ev = nullptr;
+  uint32_t tabw_queries = 0;
+  bool tabw_pending = false, persist = false;
+  ~SearchWs() {
+    if (tabw_ev) cudaEventDestroy(tabw_ev);
+    if (tabw_host) cudaFreeHost(tabw_host);
+  }
 };
 struct SearchWsCache {
   std::mutex mu;
@@ -1078,31 +1112,42 @@ static SearchWs& workspace(const DevIndex& ix, cudaStream_t st) {
   return *slot;
 }
 
-// The visited tables' evict_last accesses stay resident for good only inside
-// the L2 set-aside for persisting lines (0 by default). GRAB_L2_PERSIST=1
-// reserves the device maximum once per device: DRAM writes per cfg2 launch
-// 0.88 -> 0.07 GB and 10 % selectivity 4 % faster, but the set-aside crowds the
-// candidate rows out at wide ranges (50 %: 12 % slower), so it is opt-in.
-static void reserve_persisting_l2() {
-  static std::mutex mu;
-  static std::vector<int> done;
+// L2 regime. Narrow-range queries keep their visited table (<= 16 KB) in L2 with
+// evict_last accesses, and those stay resident only inside the L2 set-aside for
+// persisting lines: with it, a cfg2 launch at 10 % writes 0.08 GB to DRAM
+// instead of 0.89 and runs 4 % faster (5 %: 5 %). The set-aside costs wide
+// ranges a third of their L2 (20 %: 5.9 -> 7.9 ms), so it is switched per
+// launch from the previous launch's measured mean table size on the same
+// workspace (a batch of one selectivity decides after its first launch).
+struct L2Regime {
+  std::mutex mu;
+  int persist = -1;  // unknown
+  size_t max_bytes = 0;
+};
+static L2Regime& l2_regime(int dev) {
+  static L2Regime r[64];
+  return r[dev & 63];
+}
+static void set_l2_regime(bool persist) {
+  if (getenv("GRAB_L2_NO_PERSIST")) persist = false;
   int dev = 0;
   GRAB_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> g(mu);
-  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
-  done.push_back(dev);
-  if (!getenv("GRAB_L2_PERSIST")) return;  // opt-in: measured a net loss at wide ranges
-  int mx = 0;
-  if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || mx <= 0) return;
-  size_t cur = 0;
-  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-  if (cur < (size_t)mx) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx);
+  L2Regime& r = l2_regime(dev);
+  std::lock_guard<std::mutex> g(r.mu);
+  if (r.persist == (int)persist) return;
+  if (r.persist < 0) {
+    int mx = 0;
+    if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && mx > 0)
+      r.max_bytes = (size_t)mx;
+    cudaGetLastError();
+  }
+  if (r.max_bytes) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist ? r.max_bytes : 0);
   cudaGetLastError();  // best effort: never fail a search over the cache reservation
+  r.persist = (int)persist;
 }
 
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
-  reserve_persisting_l2();
   if (a.width * a.k_max > 256) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 256 not supported");
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);
@@ -1125,6 +1170,21 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.ovf_list = ovf + 1;
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
+  // L2 regime from the previous launch's table footprint (if it has landed)
+  if (!ws.tabw_host) {
+    GRAB_CUDA(cudaHostAlloc((void**)&ws.tabw_host, sizeof(unsigned long long), cudaHostAllocDefault));
+    GRAB_CUDA(cudaEventCreateWithFlags(&ws.tabw_ev, cudaEventDisableTiming));
+  }
+  if (ws.tabw_pending && cudaEventQuery(ws.tabw_ev) == cudaSuccess) {
+    const double mean_bytes = 4.0 * (double)*ws.tabw_host / std::max<uint32_t>(ws.tabw_queries, 1);
+    ws.persist = mean_bytes <= (double)GRAB_VIS_PERSIST_BYTES;
+    ws.tabw_pending = false;
+  }
+  cudaGetLastError();  // (a not-ready event query is not an error)
+  set_l2_regime(ws.persist);
+  ws.tabw.ensure(sizeof(unsigned long long), st);
+  a.tab_words = (unsigned long long*)ws.tabw.p;
+  GRAB_CUDA(cudaMemsetAsync(a.tab_words, 0, sizeof(unsigned long long), st));
 #ifdef GRAB_SEARCH_PROFILE
   {
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1132,6 +1192,12 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   }
 #endif
   launch(a, sh, ix.num_sms, st, tables, ~0ull);
+  if (!ws.tabw_pending) {  // (one readback in flight at a time)
+    GRAB_CUDA(cudaMemcpyAsync(ws.tabw_host, a.tab_words, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    GRAB_CUDA(cudaEventRecord(ws.tabw_ev, st));
+    ws.tabw_queries = a.nwork;
+    ws.tabw_pending = true;
+  }
 #ifdef GRAB_SEARCH_PROFILE
   {
     unsigned long long z[8];
@@ -1157,6 +1223,7 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   b.ovf_count = nullptr;  // cannot overflow: the table bounds every insert of max_iter iterations
   b.ovf_list = nullptr;
   b.work_ctr = a.work_ctr ? ctr + 1 : nullptr;
+  b.tab_words = nullptr;
   launch(b, big, ix.num_sms, st, big_tables, big_blocks);
   if (getenv("GRAB_DEBUG")) {
     uint32_t n_ovf = 0;
