@@ -279,25 +279,30 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
   const uint32_t lane = lane_id();
   const char* xl = reinterpret_cast<const char*>(X + lane * 4);  // this lane's first column
   const uint32_t rowb = dp * 4;
-  // rolling L2 prefetch, PF rows (~16 KB) ahead of the rows being loaded: deep
-  // enough to cover a round trip, small enough that every warp's prefetched rows
-  // stay L2-resident until used (prefetching a whole iteration of 3.75 KB rows at
-  // d = 960 overran L2 and doubled the DRAM reads)
+  // rolling L2 prefetch, PF rows (~4 KB, at least one round of G) ahead of the
+  // rows being loaded. Shallower is better once the visited tables stop
+  // competing for L2 (r02 A/B, 10 %: 16 KB 3.78 ms, 8 KB 3.72, 4 KB 3.66, none
+  // 3.93; d = 960: 29.0 -> 24.5 ms at 4 KB): prefetched rows must stay resident
+  // until used (a whole iteration at d = 960 overran L2 and doubled DRAM reads)
 #ifndef GRAB_PF_BYTES
-#define GRAB_PF_BYTES 16384u
+#define GRAB_PF_BYTES 4096u
 #endif
   constexpr uint32_t PF0 = GRAB_PF_BYTES / (NC * 512u);
   constexpr uint32_t PF = PF0 < (uint32_t)G ? (uint32_t)G : (PF0 > 32u ? 32u : PF0);
+#ifndef GRAB_NO_PF
   if (lane < PF && lane < n) {
     const float* r = X + (uint64_t)cp[lane] * dp;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(r), "r"(rowb) : "memory");
   }
+#endif
   __syncwarp();
   for (uint32_t base = 0; base < n; base += G) {
+#ifndef GRAB_NO_PF
     if (lane < (uint32_t)G && base + PF + lane < n) {
       const float* r = X + (uint64_t)cp[base + PF + lane] * dp;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(r), "r"(rowb) : "memory");
     }
+#endif
     float4 x[G][NC];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
