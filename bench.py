@@ -330,13 +330,23 @@ def cfg1_side_by_side(g, ds, dev, local, hbm, target, cpu: bool):
                 break
     ms, sp, rec = point
     torch.cuda.synchronize()
-    gi_ins = g.build_index(X, S, params, device=local)[0]
-    t0 = time.perf_counter()
-    g.insert_batch(gi_ins, Xi, Si)
-    torch.cuda.synchronize()
-    gpu_ins = len(Xi) / (time.perf_counter() - t0)
+    # one untimed insert of the same batch into another copy of the index first
+    # (a 500-vector batch is dominated by first-use costs otherwise), then the
+    # median of 3 timed inserts, each into a fresh copy of the built index
+    ins_t = []
+    for rep in range(4):
+        gi_ins = g.build_index(X, S, params, device=local)[0]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g.insert_batch(gi_ins, Xi, Si)
+        torch.cuda.synchronize()
+        if rep:
+            ins_t.append(time.perf_counter() - t0)
+        del gi_ins
+    gpu_ins = len(Xi) / sorted(ins_t)[1]
     out = {"workload": f"cfg1: {n}x{dim} fp32 low-rank-16, bucket_capacity {cap} (m={brep.m}), {nq} range queries "
-                       f"at 10% selectivity, k=10; insert = one {len(Xi)}-vector batch",
+                       f"at 10% selectivity, k=10; insert = one {len(Xi)}-vector batch (GPU: median of 3 into "
+                       f"fresh copies of the index after one untimed)",
            "gpu": {"build_s": round(sorted(times)[1], 4), "qps": round(nq / (ms / 1e3), 1),
                    "recall_at_10": round(rec, 4), "itopk": sp.itopk, "search_width": 4,
                    "max_iterations": sp.max_iterations, "insert_vectors_per_s": round(gpu_ins, 1),

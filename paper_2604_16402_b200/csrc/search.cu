@@ -1085,7 +1085,8 @@ struct SearchWs {
   unsigned long long* tabw_host = nullptr;  // pinned
   cudaEvent_t tabw_ev = nullptr;
   uint32_t tabw_queries = 0;
-  bool tabw_pending = false, persist = false;
+  bool tabw_pending = false;
+  int persist = -1;  // regime this workspace's last launch asked for (-1: no evidence yet)
   ~SearchWs() {
     if (tabw_ev) cudaEventDestroy(tabw_ev);
     if (tabw_host) cudaFreeHost(tabw_host);
@@ -1182,11 +1183,13 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   }
   if (ws.tabw_pending && cudaEventQuery(ws.tabw_ev) == cudaSuccess) {
     const double mean_bytes = 4.0 * (double)*ws.tabw_host / std::max<uint32_t>(ws.tabw_queries, 1);
-    ws.persist = mean_bytes <= (double)GRAB_VIS_PERSIST_BYTES;
+    ws.persist = mean_bytes <= (double)GRAB_VIS_PERSIST_BYTES ? 1 : 0;
     ws.tabw_pending = false;
   }
   cudaGetLastError();  // (a not-ready event query is not an error)
-  set_l2_regime(ws.persist);
+  // (a workspace without evidence keeps the device's current regime: toggling the
+  // set-aside is a device-wide reconfiguration, not free)
+  if (ws.persist >= 0) set_l2_regime(ws.persist == 1);
   ws.tabw.ensure(sizeof(unsigned long long), st);
   a.tab_words = (unsigned long long*)ws.tabw.p;
   GRAB_CUDA(cudaMemsetAsync(a.tab_words, 0, sizeof(unsigned long long), st));
