@@ -235,6 +235,13 @@ GRAB_API int grab_scc_count(const grab_index* h, uint64_t live_count, uint64_t* 
 /* the same over an explicit slot-space adjacency (host pointer, rows x k_max) */
 GRAB_API int grab_scc_count_raw(const uint32_t* adjacency, uint64_t rows, uint32_t k_max, uint64_t live_count,
                                 uint64_t* out);
+/* _reverse_merge_topk (builder.py:338-361) over an explicit graph (host
+ * pointers): rows X [n x dim] f32, graph [n x k] slot ids (SENTINEL = none,
+ * k <= k_g); union with the reverse edges, dedup, the k_g nearest per row by
+ * (f64 distance, slot) -> out [n x k_g] (SENTINEL padded). The kernels of the
+ * device build's global pass. */
+GRAB_API int grab_reverse_merge_raw(int device, const float* X, uint64_t n, uint32_t dim, const uint32_t* graph,
+                                    uint32_t k, uint32_t k_g, uint32_t* out);
 
 /* ---- bucket-range sharded search (no reference counterpart:
  * the reference is single-process, so these replace nothing and follow the

@@ -102,6 +102,7 @@ _SIGS = {
     "grab_shard_pack": (C.c_int, [u64, P, P, P, P, u32, u32, u32, P, P, P]),
     "grab_merge_topk": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, P]),
     "grab_shard_pack_p2p": (C.c_int, [u64, P, P, P, P, u32, u32, u32, u32, P, P, P]),
+    "grab_reverse_merge_raw": (C.c_int, [C.c_int, P, u64, u32, P, u32, u32, P]),
     "grab_shard_sync_bytes": (u64, [u32]),
     "grab_shard_pack_p2p_sync": (C.c_int, [u32, u64, P, P, P, P, u32, u32, u32, u32, P, P, P, P, u64, P, P]),
     "grab_merge_topk_p2p": (C.c_int, [u32, u32, u32, u32, P, P, P, P, P, u32, P, P, u64, P]),

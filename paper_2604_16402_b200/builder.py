@@ -157,6 +157,37 @@ def reinforce_reachability(index: GraphIndex) -> int:
     return int(added.value)
 
 
+def _random_init_graph(X, k: int, rng: np.random.Generator):
+    """builder.py:330-335: ``rng.integers(0, n - 1, (n, k))`` shifted past the row
+    itself, and the edges' squared distances. The draw consumes the caller's
+    numpy Generator (its state advances exactly like the reference's); the
+    distances are computed on the device (f64, returned as f32)."""
+    X = np.asarray(X, dtype=np.float32)
+    n = len(X)
+    graph = rng.integers(0, n - 1, size=(n, k), dtype=np.int64)
+    graph[graph >= np.arange(n)[:, None]] += 1  # avoid self
+    from .api import sq_distances
+    dists = np.stack([sq_distances(X[v], X[graph[v]]) for v in range(n)]).astype(np.float32) if n else \
+        np.empty((0, k), np.float32)
+    return graph, dists
+
+
+def _reverse_merge_topk(graph, X, k_g: int, block: int = 4096) -> np.ndarray:
+    """builder.py:338-361: union with the reverse edges, dedup, the k_g closest
+    per node by (dist, slot) -- the device build's global-pass kernels over this
+    graph (``grab_reverse_merge_raw``; ``block`` is the reference's host
+    blocking and has no meaning here)."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    g = np.asarray(graph)
+    n, k = g.shape
+    g32 = np.where((g >= 0) & (g < n), g, SENTINEL).astype("<u4")
+    out = np.empty((n, int(k_g)), "<u4")
+    if n:
+        L.check(L.lib.grab_reverse_merge_raw(0, L.ptr(X), n, X.shape[1], L.ptr(np.ascontiguousarray(g32)), k,
+                                             int(k_g), L.ptr(out)))
+    return out.astype(np.int64)
+
+
 def interleave_merge(forward, reverse, k_max: int) -> list:
     """builder.py:130-153: forward[0], reverse[0], forward[1], ... without repeats."""
     out: list = []

@@ -331,6 +331,100 @@ __global__ void k_union_topk(const uint32_t* rows, uint64_t nrows, const uint32_
   for (uint32_t i = lane; i < K; i += 32) G[(uint64_t)p * K + i] = lp[i];
 }
 
+__global__ void k_iota(uint32_t* out, uint64_t n) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)i;
+}
+
+// f64 distance of every edge (warp per row, the library's reduction tree);
+// SENTINEL / self / out-of-range entries become SENTINEL
+__global__ void k_edge_dists_f64(const float* X, uint32_t dp, uint64_t n, const uint32_t* g, uint32_t k,
+                                 uint32_t* gf, double* gd) {
+  const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  if (v >= n) return;
+  for (uint32_t j = 0; j < k; ++j) {
+    const uint32_t u = g[v * k + j];
+    const bool ok = u != kSentinel && u < n && u != v;  // warp-uniform
+    if (!ok) {
+      if (lane == 0) gf[v * k + j] = kSentinel;
+      continue;
+    }
+    double acc = 0.0;
+    for (uint32_t col = lane * 4; col < dp; col += 128)
+      acc = sq4(*reinterpret_cast<const float4*>(X + (uint64_t)u * dp + col),
+                *reinterpret_cast<const float4*>(X + v * dp + col), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      gf[v * k + j] = u;
+      gd[v * k + j] = acc;
+    }
+  }
+}
+
+__global__ void k_identity_attr(Attr* a, uint64_t n) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    a[i].s = 0.f;
+    a[i].slot = (uint32_t)i;
+  }
+}
+
+// _reverse_merge_topk (builder.py:338-361) over an explicit graph: the same
+// reverse lists + union / dedup / top-k_g kernels the global pass runs (f64
+// edge distances), on rows X[n x dim] with slot = row index. Host pointers.
+void reverse_merge_raw(const float* X, uint64_t n, uint32_t dim, const uint32_t* graph, uint32_t k, uint32_t k_g,
+                       uint32_t* out) {
+  if (k > k_g) throw Error(GRAB_ERR_VALUE, "reverse merge: graph width above k_g");
+  cudaStream_t st = 0;
+  Scratch S(st);
+  const uint32_t dp = (dim + 3) / 4 * 4;
+  float* dX = S.alloc<float>(std::max<uint64_t>(n, 1) * dp);
+  GRAB_CUDA(cudaMemsetAsync(dX, 0, std::max<uint64_t>(n, 1) * dp * 4, st));
+  GRAB_CUDA(cudaMemcpy2DAsync(dX, dp * 4, X, dim * 4, dim * 4, n, cudaMemcpyHostToDevice, st));
+  const uint64_t ne = n * (uint64_t)k;
+  uint32_t* g = S.alloc<uint32_t>(std::max<uint64_t>(ne, 1));
+  GRAB_CUDA(cudaMemcpyAsync(g, graph, ne * 4, cudaMemcpyHostToDevice, st));
+  uint32_t* gf = S.alloc<uint32_t>(std::max<uint64_t>(ne, 1));
+  double* gd = S.alloc<double>(std::max<uint64_t>(ne, 1));
+  k_edge_dists_f64<<<(unsigned)div_up(n * 32, 256), 256, 0, st>>>(dX, dp, n, g, k, gf, gd);
+  GRAB_CHECK_LAUNCH();
+  Attr* attr = S.alloc<Attr>(std::max<uint64_t>(n, 1));
+  k_identity_attr<<<(unsigned)div_up(n, 256), 256, 0, st>>>(attr, n);
+  GRAB_CHECK_LAUNCH();
+  uint32_t* cnt = S.alloc<uint32_t>(n + 1);
+  uint32_t* off = S.alloc<uint32_t>(n + 1);
+  uint32_t* fill = S.alloc<uint32_t>(std::max<uint64_t>(n, 1));
+  uint32_t* prow = S.alloc<uint32_t>(std::max<uint64_t>(n, 1));
+  k_iota<<<(unsigned)div_up(n, 256), 256, 0, st>>>(prow, n);
+  GRAB_CHECK_LAUNCH();
+  GRAB_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * 4, st));
+  GRAB_CUDA(cudaMemsetAsync(fill, 0, n * 4, st));
+  k_count_rev<<<(unsigned)div_up(ne, 256), 256, 0, st>>>(gf, n, k, cnt);
+  GRAB_CHECK_LAUNCH();
+  exclusive_scan_u32(cnt, off, n + 1, st);
+  uint32_t nrev = 0;
+  GRAB_CUDA(cudaMemcpyAsync(&nrev, off + n, 4, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+  uint32_t* rsrc = S.alloc<uint32_t>(std::max<uint32_t>(nrev, 1));
+  double* rdist = S.alloc<double>(std::max<uint32_t>(nrev, 1));
+  k_scatter_rev<<<(unsigned)div_up(ne, 256), 256, 0, st>>>(gf, gd, prow, n, k, off, fill, rsrc, rdist);
+  GRAB_CHECK_LAUNCH();
+  // k_union_topk reads the forward rows with stride K = k_g: re-pack them
+  uint32_t* gfk = S.alloc<uint32_t>(std::max<uint64_t>(n * (uint64_t)k_g, 1));
+  double* gdk = S.alloc<double>(std::max<uint64_t>(n * (uint64_t)k_g, 1));
+  GRAB_CUDA(cudaMemsetAsync(gfk, 0xFF, n * (uint64_t)k_g * 4, st));
+  GRAB_CUDA(cudaMemcpy2DAsync(gfk, (size_t)k_g * 4, gf, (size_t)k * 4, (size_t)k * 4, n, cudaMemcpyDeviceToDevice, st));
+  GRAB_CUDA(cudaMemcpy2DAsync(gdk, (size_t)k_g * 8, gd, (size_t)k * 8, (size_t)k * 8, n, cudaMemcpyDeviceToDevice, st));
+  uint32_t* G = S.alloc<uint32_t>(std::max<uint64_t>(n * (uint64_t)k_g, 1));
+  const uint32_t wpb = 4;
+  const size_t smem = (size_t)wpb * k_g * 16;
+  k_union_topk<<<(unsigned)div_up(n, wpb), 32 * wpb, smem, st>>>(prow, n, gfk, gdk, k_g, off, rsrc, rdist, attr, G);
+  GRAB_CHECK_LAUNCH();
+  GRAB_CUDA(cudaMemcpyAsync(out, G, n * (uint64_t)k_g * 4, cudaMemcpyDeviceToHost, st));
+  GRAB_CUDA(cudaStreamSynchronize(st));
+}
+
 // ---------------------------------------------------------------- fuse
 // fuse_remote_edges (builder.py:396-452); one thread per node.
 __global__ void k_fuse(const uint32_t* rows, uint64_t nrows, const uint32_t* G, uint32_t k_g, const Attr* attr,
@@ -631,12 +725,8 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
     GRAB_CUDA(cudaMemsetAsync(fill, 0, ix.phys_cap * 4, st));
     // fwd is indexed by phys row; iterate all phys rows (invalid rows are all-SENTINEL)
     uint32_t* prow = S.alloc<uint32_t>(ix.phys_cap);
-    {
-      std::vector<uint32_t> h(ix.phys_cap);
-      for (uint64_t i = 0; i < ix.phys_cap; ++i) h[i] = (uint32_t)i;
-      GRAB_CUDA(cudaMemcpyAsync(prow, h.data(), ix.phys_cap * 4, cudaMemcpyHostToDevice, st));
-      GRAB_CUDA(cudaStreamSynchronize(st));
-    }
+    k_iota<<<(unsigned)div_up(ix.phys_cap, 256), 256, 0, st>>>(prow, ix.phys_cap);
+    GRAB_CHECK_LAUNCH();
     uint64_t ne = ix.phys_cap * (uint64_t)K;
     k_count_rev<<<(unsigned)div_up(ne, 256), 256, 0, st>>>(fwd, ix.phys_cap, K, cnt);
     GRAB_CHECK_LAUNCH();
@@ -699,12 +789,8 @@ void build_graph_device(DevIndex& ix, uint64_t n, uint32_t k_g, uint32_t refine_
     uint32_t* off = S.alloc<uint32_t>(ix.phys_cap + 1);
     uint32_t* fill = S.alloc<uint32_t>(ix.phys_cap);
     uint32_t* prow = S.alloc<uint32_t>(ix.phys_cap);
-    {
-      std::vector<uint32_t> h(ix.phys_cap);
-      for (uint64_t i = 0; i < ix.phys_cap; ++i) h[i] = (uint32_t)i;
-      GRAB_CUDA(cudaMemcpyAsync(prow, h.data(), ix.phys_cap * 4, cudaMemcpyHostToDevice, st));
-      GRAB_CUDA(cudaStreamSynchronize(st));
-    }
+    k_iota<<<(unsigned)div_up(ix.phys_cap, 256), 256, 0, st>>>(prow, ix.phys_cap);
+    GRAB_CHECK_LAUNCH();
     GRAB_CUDA(cudaMemsetAsync(cnt, 0, (ix.phys_cap + 1) * 4, st));
     GRAB_CUDA(cudaMemsetAsync(fill, 0, ix.phys_cap * 4, st));
     uint64_t ne = ix.phys_cap * (uint64_t)k_g;

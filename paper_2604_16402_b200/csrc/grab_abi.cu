@@ -727,6 +727,21 @@ extern "C" int grab_bucket_select_raw(const float* boundaries, uint32_t m, const
   });
 }
 
+namespace grab {
+void reverse_merge_raw(const float* X, uint64_t n, uint32_t dim, const uint32_t* graph, uint32_t k, uint32_t k_g,
+                       uint32_t* out);  // build.cu
+}
+
+extern "C" int grab_reverse_merge_raw(int device, const float* X, uint64_t n, uint32_t dim, const uint32_t* graph,
+                                      uint32_t k, uint32_t k_g, uint32_t* out) {
+  return guarded([&] {
+    if (dim < 1 || k_g < 1) throw Error(GRAB_ERR_VALUE, "dim and k_g must be >= 1");
+    if (n >= 0xFFFFFFFFull) throw Error(GRAB_ERR_VALUE, "n exceeds the u32 id space");
+    GRAB_CUDA(cudaSetDevice(device));
+    if (n) reverse_merge_raw(X, n, dim, graph, k, k_g, out);
+  });
+}
+
 extern "C" int grab_sq_distances(const float* q, const float* rows, uint64_t n, uint32_t dim, double* out) {
   return guarded([&] {
     if (!n) return;

@@ -20,13 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITE = os.path.join(ROOT, "baseline", "_ref_tests")
 
 # test id -> why the drop-in does not (and should not) pass it
-JUSTIFIED = {
-    "test_builder.py::test_global_graph_zero_rounds_is_init_plus_reverse_merge":
-        "imports the reference's private numpy helpers _random_init_graph / _reverse_merge_topk "
-        "(builder.py:270-335), which have no counterpart on the device path; the same property "
-        "(pass 2 with 0 rounds = random init + reverse merge) is pinned row for row against the "
-        "reference in tests/test_gpu_build.py::test_nn_descent_global_pass_matches_reference",
-}
+JUSTIFIED: dict = {}
 
 
 def test_reference_suite_passes_on_the_device_package(tmp_path):
