@@ -274,21 +274,28 @@ struct GroupOf {
 // lane sits past the row end); otherwise every chunk load is predicated.
 template <int NC, bool FULL>
 __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __restrict__ X, uint32_t dp,
-                                      const uint32_t* cp, double* cd, uint32_t n) {
+                                      const uint32_t* cp, double* cd, uint32_t n, bool deep_pf) {
   constexpr int G = GroupOf<NC>::G;
   const uint32_t lane = lane_id();
   const char* xl = reinterpret_cast<const char*>(X + lane * 4);  // this lane's first column
   const uint32_t rowb = dp * 4;
-  // rolling L2 prefetch, PF rows (~4 KB, at least one round of G) ahead of the
-  // rows being loaded. Shallower is better once the visited tables stop
-  // competing for L2 (r02 A/B, 10 %: 16 KB 3.78 ms, 8 KB 3.72, 4 KB 3.66, none
-  // 3.93; d = 960: 29.0 -> 24.5 ms at 4 KB): prefetched rows must stay resident
-  // until used (a whole iteration at d = 960 overran L2 and doubled DRAM reads)
+  // rolling L2 prefetch, PF rows ahead of the rows being loaded. Bitmap-mode
+  // queries (the visited span fits the warp's table) prefetch ~4 KB (at least
+  // one round of G): shallower is better once their tables stay in L2 (r02 A/B,
+  // cfg2 10 %: 16 KB 3.78 ms, 8 KB 3.72, 4 KB 3.66, none 3.93; d = 960: 29.0 ->
+  // 24.5 ms). Hash-mode queries (wide spans on large indexes: cfg5's 12.5M-row
+  // shards) keep ~16 KB ahead: 130K -> 247K QPS there. Prefetched rows must stay
+  // resident until used (a whole iteration at d = 960 overran L2).
 #ifndef GRAB_PF_BYTES
 #define GRAB_PF_BYTES 4096u
 #endif
-  constexpr uint32_t PF0 = GRAB_PF_BYTES / (NC * 512u);
-  constexpr uint32_t PF = PF0 < (uint32_t)G ? (uint32_t)G : (PF0 > 32u ? 32u : PF0);
+#ifndef GRAB_PF_BYTES_DEEP
+#define GRAB_PF_BYTES_DEEP 16384u
+#endif
+  constexpr uint32_t PFS0 = GRAB_PF_BYTES / (NC * 512u), PFD0 = GRAB_PF_BYTES_DEEP / (NC * 512u);
+  constexpr uint32_t PFS = PFS0 < (uint32_t)G ? (uint32_t)G : (PFS0 > 32u ? 32u : PFS0);
+  constexpr uint32_t PFD = PFD0 < (uint32_t)G ? (uint32_t)G : (PFD0 > 32u ? 32u : PFD0);
+  const uint32_t PF = deep_pf ? PFD : PFS;
 #ifndef GRAB_NO_PF
   if (lane < PF && lane < n) {
     const float* r = X + (uint64_t)cp[lane] * dp;
@@ -691,7 +698,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
       uint32_t fu = 0;  // every queue entry before fu is expanded
       if (ns > 0) {
         pad_cands(cp, ns);
-        score<NC, FULL>(qr, a.X, a.dp, cp, cd, ns);
+        score<NC, FULL>(qr, a.X, a.dp, cp, cd, ns, !vis.bm);
         dist_evals = seed_evals = ns;
         L = admit(qe, cd, cs, cp, 0, ns, sh.itopk, fu);
         PROF(0)
@@ -851,7 +858,7 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
           if (nc == 0) continue;
           dist_evals += nc;
           pad_cands(cp, nc);
-          score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc);
+          score<NC, FULL>(qr, a.X, a.dp, cp, cd, nc, !vis.bm);
           PROF(5)
           L = admit(qe, cd, cs, cp, L, nc, sh.itopk, fu);
           PROF(6)
