@@ -687,7 +687,6 @@ __global__ void __launch_bounds__(128, NC >= 16 ? 3 : (EPL >= 8 ? 4 : GRAB_SEARC
       vis.bm = vis.nbits <= (32u << vlg);
       vis.pol = vis_make_policy(vis.clear_words_n() * 4u <= GRAB_VIS_PERSIST_BYTES);
       vis_clear(vtab, vis.clear_words_n(), vis.pol);
-      if (lane == 0 && a.tab_words) atomicAdd(a.tab_words, (unsigned long long)vis.clear_words_n());
       __syncwarp();
       const uint64_t seed = a.seeds ? a.seeds[qi] : derive_query_seed(a.seed_base, a.ordinal0 + qi);
       const uint32_t ns = sample_seeds(a, dd, cp, cs, vis, lo_b, hi_b, lo_f, hi_f, seed, &attempts);
@@ -1087,17 +1086,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
 // order makes the reuse safe without host synchronization).
 struct SearchWs {
   std::mutex mu;  // host-side: one enqueue at a time per stream (threads may share a stream)
-  DBufLite tables, big_tables, ovf, ctr, tabw;
-  // the previous launch's visited-table footprint, copied back asynchronously
-  unsigned long long* tabw_host = nullptr;  // pinned
-  cudaEvent_t tabw_ev = nullptr;
-  uint32_t tabw_queries = 0;
-  bool tabw_pending = false;
-  int persist = -1;  // regime this workspace's last launch asked for (-1: no evidence yet)
-  ~SearchWs() {
-    if (tabw_ev) cudaEventDestroy(tabw_ev);
-    if (tabw_host) cudaFreeHost(tabw_host);
-  }
+  DBufLite tables, big_tables, ovf, ctr;
 };
 struct SearchWsCache {
   std::mutex mu;
@@ -1125,42 +1114,37 @@ static SearchWs& workspace(const DevIndex& ix, cudaStream_t st) {
   return *slot;
 }
 
-// L2 regime. Narrow-range queries keep their visited table (<= 16 KB) in L2 with
-// evict_last accesses, and those stay resident only inside the L2 set-aside for
-// persisting lines: with it, a cfg2 launch at 10 % writes 0.08 GB to DRAM
-// instead of 0.89 and runs 4 % faster (5 %: 5 %). The set-aside costs wide
-// ranges a third of their L2 (20 %: 5.9 -> 7.9 ms), so it is switched per
-// launch from the previous launch's measured mean table size on the same
-// workspace (a batch of one selectivity decides after its first launch).
-struct L2Regime {
-  std::mutex mu;
-  int persist = -1;  // unknown
-  size_t max_bytes = 0;
-};
-static L2Regime& l2_regime(int dev) {
-  static L2Regime r[64];
-  return r[dev & 63];
-}
-static void set_l2_regime(bool persist) {
-  if (getenv("GRAB_L2_NO_PERSIST")) persist = false;
+// L2 set-aside for persisting lines. Narrow-range queries keep their visited
+// table (<= 16 KB) in L2 with evict_last accesses, and those stay resident only
+// inside the persisting set-aside. A fixed 48 MB set-aside, reserved once per
+// device, is the measured balance (r02, cfg2; ms per 10K queries at 0 / 32 /
+// 48 / 64 MB): 10 %: 3.94 / 3.78 / 3.70 / 3.66; 5 %: 2.78 / 2.62 / 2.59 / 2.59;
+// 20 %: 5.76 / 5.75 / 5.82 / 6.85; 50 %: 10.0 / 10.0 / 10.2 / 12.6. (Switching
+// the set-aside per launch from the batch's table sizes was tried: reconfiguring
+// it while kernels run stalled a launch by 22 ms.) GRAB_L2_PERSIST_MB overrides
+// the size (0 = none).
+static void reserve_persisting_l2() {
+  static std::mutex mu;
+  static std::vector<int> done;
   int dev = 0;
   GRAB_CUDA(cudaGetDevice(&dev));
-  L2Regime& r = l2_regime(dev);
-  std::lock_guard<std::mutex> g(r.mu);
-  if (r.persist == (int)persist) return;
-  if (r.persist < 0) {
-    int mx = 0;
-    if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && mx > 0)
-      r.max_bytes = (size_t)mx;
+  std::lock_guard<std::mutex> g(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  done.push_back(dev);
+  size_t want = (size_t)48 << 20;
+  if (const char* e = getenv("GRAB_L2_PERSIST_MB")) want = (size_t)atoi(e) << 20;
+  int mx = 0;
+  if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || mx <= 0) {
     cudaGetLastError();
+    return;
   }
-  if (r.max_bytes) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist ? r.max_bytes : 0);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(want, (size_t)mx));
   cudaGetLastError();  // best effort: never fail a search over the cache reservation
-  r.persist = (int)persist;
 }
 
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
+  reserve_persisting_l2();
   if (a.width * a.k_max > 256) throw Error(GRAB_ERR_VALUE, "search_width * k_max > 256 not supported");
   if (ix.phys_cap >= kExpanded) throw Error(GRAB_ERR_CAPACITY, "search needs phys ids < 2^31");
   ensure_adja(ix, st);
@@ -1183,23 +1167,6 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.ovf_list = ovf + 1;
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
-  // L2 regime from the previous launch's table footprint (if it has landed)
-  if (!ws.tabw_host) {
-    GRAB_CUDA(cudaHostAlloc((void**)&ws.tabw_host, sizeof(unsigned long long), cudaHostAllocDefault));
-    GRAB_CUDA(cudaEventCreateWithFlags(&ws.tabw_ev, cudaEventDisableTiming));
-  }
-  if (ws.tabw_pending && cudaEventQuery(ws.tabw_ev) == cudaSuccess) {
-    const double mean_bytes = 4.0 * (double)*ws.tabw_host / std::max<uint32_t>(ws.tabw_queries, 1);
-    ws.persist = mean_bytes <= (double)GRAB_VIS_PERSIST_BYTES ? 1 : 0;
-    ws.tabw_pending = false;
-  }
-  cudaGetLastError();  // (a not-ready event query is not an error)
-  // (a workspace without evidence keeps the device's current regime: toggling the
-  // set-aside is a device-wide reconfiguration, not free)
-  if (ws.persist >= 0) set_l2_regime(ws.persist == 1);
-  ws.tabw.ensure(sizeof(unsigned long long), st);
-  a.tab_words = (unsigned long long*)ws.tabw.p;
-  GRAB_CUDA(cudaMemsetAsync(a.tab_words, 0, sizeof(unsigned long long), st));
 #ifdef GRAB_SEARCH_PROFILE
   {
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1207,12 +1174,6 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   }
 #endif
   launch(a, sh, ix.num_sms, st, tables, ~0ull);
-  if (!ws.tabw_pending) {  // (one readback in flight at a time)
-    GRAB_CUDA(cudaMemcpyAsync(ws.tabw_host, a.tab_words, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    GRAB_CUDA(cudaEventRecord(ws.tabw_ev, st));
-    ws.tabw_queries = a.nwork;
-    ws.tabw_pending = true;
-  }
 #ifdef GRAB_SEARCH_PROFILE
   {
     unsigned long long z[8];
@@ -1238,7 +1199,6 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   b.ovf_count = nullptr;  // cannot overflow: the table bounds every insert of max_iter iterations
   b.ovf_list = nullptr;
   b.work_ctr = a.work_ctr ? ctr + 1 : nullptr;
-  b.tab_words = nullptr;
   launch(b, big, ix.num_sms, st, big_tables, big_blocks);
   if (getenv("GRAB_DEBUG")) {
     uint32_t n_ovf = 0;

@@ -38,9 +38,6 @@ struct SearchArgs {
   // if set, warps claim work items dynamically (atomicAdd) instead of the static
   // stride: queries differ in cost, so this evens out the grid's tail
   uint32_t* work_ctr;
-  // if set, every query adds its visited-table words (bitmap span or hash size):
-  // read back after the launch to pick the next launch's L2 regime
-  unsigned long long* tab_words;
   // outputs (indexed by query id)
   int64_t* out_slots;
   double* out_dists;
