@@ -114,6 +114,102 @@ __device__ __forceinline__ double dist_batch(const RowRegs<NC>& r, const float* 
   return reduce_scatter<G>(part);
 }
 
+// f32 screen of the same G rows: direct differences, one FMA chain per lane and
+// the same pairing tree in f32. Within kScreenRel * value of the exact (f64)
+// distance: <= (dp / 32 + 8) roundings of 2^-24 relative each, all terms >= 0.
+template <int G>
+__device__ __forceinline__ float reduce_scatter_f32(float (&p)[G]) {
+  const uint32_t lane = threadIdx.x & 31u;
+  if constexpr (G == 1) {
+    float t = p[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+    return t;
+  } else {
+    constexpr int H = G / 2;
+    float q[H];
+    const bool hi = (lane & 16u) != 0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const float send = hi ? p[j] : p[H + j];
+      const float keep = hi ? p[H + j] : p[j];
+      q[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 16);
+    }
+    if constexpr (H == 1) {
+      float t = q[0];
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+      return t;
+    } else {
+      constexpr int H2 = H / 2;
+      float r[H2];
+      const bool hi2 = (lane & 8u) != 0;
+#pragma unroll
+      for (int j = 0; j < H2; ++j) {
+        const float send = hi2 ? q[j] : q[H2 + j];
+        const float keep = hi2 ? q[H2 + j] : q[j];
+        r[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 8);
+      }
+      if constexpr (H2 == 1) {
+        float t = r[0];
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+        return t;
+      } else {
+        const bool hi3 = (lane & 4u) != 0;
+        const float send = hi3 ? r[0] : r[1];
+        const float keep = hi3 ? r[1] : r[0];
+        float t = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 4);
+        t += __shfl_xor_sync(0xFFFFFFFFu, t, 2);
+        t += __shfl_xor_sync(0xFFFFFFFFu, t, 1);
+        return t;
+      }
+    }
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ float dist_batch_f32(const RowRegs<NC>& r, const float* X, uint32_t dp,
+                                                const uint32_t (&p)[Batch<NC>::G], const bool (&ok)[Batch<NC>::G]) {
+  constexpr int G = Batch<NC>::G;
+  const uint32_t lane = lane_id();
+  float4 x[G][NC];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t col = (c * 32 + lane) * 4;
+      x[g][c] = (ok[g] && col < dp) ? ldg_nc_f4(X + (uint64_t)p[g] * dp + col) : make_float4(0, 0, 0, 0);
+    }
+  float part[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t col = (c * 32 + lane) * 4;
+      if (col < dp) {
+        const float4 q = r.v[c];
+        float d = x[g][c].x - q.x;
+        acc = fmaf(d, d, acc);
+        d = x[g][c].y - q.y;
+        acc = fmaf(d, d, acc);
+        d = x[g][c].z - q.z;
+        acc = fmaf(d, d, acc);
+        d = x[g][c].w - q.w;
+        acc = fmaf(d, d, acc);
+      }
+    }
+    part[g] = acc;
+  }
+  return reduce_scatter_f32<G>(part);
+}
+
+// relative error bound of the f32 screen for rows of dp floats (generous: 4x)
+__device__ __forceinline__ double screen_rel(uint32_t dp) {
+  return fmax(ldexp(1.0, -16), (double)(dp / 32 + 8) * ldexp(1.0, -22));
+}
+
 // ------------------------------------------------------------- shared counters
 struct InsertCounters {
   unsigned long long forward_accepted, forward_rejected, reverse_accepted, reverse_rejected;
@@ -273,8 +369,13 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
     }
     __syncwarp();
     {
-      // G candidate rows in flight per round; reduce_scatter is bit-identical to row_dist
+      // near[j] only ever meets de_j (live iff de_j < near[j]), so what a
+      // measurement must decide is dist(s, j) <= de_j. G rows per round are
+      // screened in f32 (half the FP64 work); a row whose screen value is
+      // within the error bound of de_j is re-measured exactly (row_dist: the
+      // f64 tree) -- the decisions, and so the rows, are the f64 ones.
       constexpr int G = Batch<NC>::G, SH = Batch<NC>::SH;
+      const double rel = screen_rel(dp);
       for (uint32_t a0 = 0; a0 < na; a0 += G) {
         uint32_t p[G];
         bool ok[G];
@@ -283,11 +384,26 @@ __global__ void __launch_bounds__(128, NC <= 2 ? GRAB_INSERT_MINB : 1) k_forward
           ok[g] = a0 + g < na;
           p[g] = ok[g] ? cph[alv[a0 + g]] : 0u;
         }
-        const double dsum = dist_batch<NC>(r, X, dp, p, ok);
+        const float fsum = dist_batch_f32<NC>(r, X, dp, p, ok);
         const uint32_t a = a0 + (lane >> SH);
+        bool unsure = false;
         if ((lane & ((1u << SH) - 1)) == 0 && a < na) {
           const uint32_t j = alv[a];
-          if (dsum < near[j]) near[j] = dsum;
+          const double dj = cd[j];
+          const double dej = cs[j] >= start ? alpha2 * dj : dj;
+          const double f = (double)fsum, m = rel * fmax(f, dej);
+          if (f < dej - m)
+            near[j] = 0.0;  // dist <= de_j: j is rejected
+          else if (!(f > dej + m))
+            unsure = true;  // (else dist > de_j: no decision changes)
+        }
+        uint32_t um = __ballot_sync(0xFFFFFFFFu, unsure);
+        while (um) {  // exact re-measure of the close calls, one row at a time
+          const uint32_t src = __ffs(um) - 1;
+          um &= um - 1;
+          const uint32_t j = alv[a0 + (src >> SH)];
+          const double d = row_dist<NC>(r, X, dp, cph[j]);
+          if (lane == 0 && d < near[j]) near[j] = d;
         }
       }
     }
