@@ -533,9 +533,45 @@ __global__ void k_rewire(const unsigned long long* keys, const double* dvq, uint
       load_row<NC>(rq, X, dp, pq);
       bool ok = true;
       constexpr int G = Batch<NC>::G, SH = Batch<NC>::SH;
+      const double rel = screen_rel(dp);
+      // reject iff some neighbour n has dist(q, n) <= deff: screened in f32,
+      // rows within the error bound of deff re-measured exactly (f64 tree)
       for (uint32_t j0 = 0; j0 < K && ok; j0 += G) {
-        const double dj = dist_entries<NC>(rq, X, dp, e, j0, K);
-        ok = !__any_sync(0xFFFFFFFFu, (lane & ((1u << SH) - 1)) == 0 && j0 + (lane >> SH) < K && !(deff < dj));
+        uint32_t p[G];
+        bool okg[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t j = j0 + g;
+          p[g] = __shfl_sync(0xFFFFFFFFu, (j & 32) ? e[1] : e[0], j & 31);
+          okg[g] = j < K && p[g] != kSentinel;
+        }
+        const float f = dist_batch_f32<NC>(rq, X, dp, p, okg);
+        bool okl = false;
+        uint32_t pl = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          okl = (lane >> SH) == (uint32_t)g ? okg[g] : okl;
+          pl = (lane >> SH) == (uint32_t)g ? p[g] : pl;
+        }
+        bool fail = false, unsure = false;
+        if ((lane & ((1u << SH) - 1)) == 0 && okl) {
+          const double fd = (double)f, m = rel * fmax(fd, deff);
+          if (fd < deff - m)
+            fail = true;
+          else if (!(fd > deff + m))
+            unsure = true;
+        }
+        if (__any_sync(0xFFFFFFFFu, fail)) {
+          ok = false;
+          break;
+        }
+        uint32_t um = __ballot_sync(0xFFFFFFFFu, unsure);
+        while (um && ok) {
+          const uint32_t src = __ffs(um) - 1;
+          um &= um - 1;
+          const double d = row_dist<NC>(rq, X, dp, __shfl_sync(0xFFFFFFFFu, pl, src));
+          ok = deff < d;
+        }
       }
       if (!ok) {
         ++rej;
