@@ -114,3 +114,21 @@ def test_derive_query_seed_matches_seedsequence(g):
     for base, o in [(0, 0), (11, 3), (2 ** 64 - 1, 7), (5, 2 ** 31)]:
         want = int(np.random.SeedSequence([base, o]).generate_state(1, np.uint64)[0])
         assert g.derive_query_seed(base, o) == want
+
+
+def test_insert_report_rewired_rows_behave_like_a_sorted_list():
+    """InsertReport.rewired_rows (updater.py:42,261: sorted(rewired)) is returned as
+    an array-backed sequence; every list use the reference and its tests make works."""
+    from paper_2604_16402_b200.api import InsertReport, RowList
+    rows = np.array([3, 7, 7000000, 2 ** 31 + 5], dtype=np.uint32)
+    rl = RowList(rows)
+    assert len(rl) == 4 and list(rl) == [3, 7, 7000000, 2 ** 31 + 5]
+    assert rl == [3, 7, 7000000, 2 ** 31 + 5] and rl == (3, 7, 7000000, 2 ** 31 + 5)
+    assert not (rl == [3, 7]) and rl != [3, 7, 7000000, 6]
+    assert rl[0] == 3 and rl[-1] == 2 ** 31 + 5 and rl[1:3] == [7, 7000000]
+    assert 7 in rl and 8 not in rl and set(rl) == {3, 7, 7000000, 2 ** 31 + 5}
+    assert sorted(rl) == rl.tolist() and np.array_equal(np.asarray(rl), rows.astype(np.int64))
+    assert {1, 3}.issubset(set(rl)) is False and {3, 7}.issubset(set(rl))
+    rep = InsertReport(batch_size=2, rewired_rows=rl)
+    assert rep.to_dict()["rewired_rows"] == [3, 7, 7000000, 2 ** 31 + 5]
+    assert RowList(np.empty(0, np.uint32)) == [] and len(RowList(np.empty(0, np.uint32))) == 0
