@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // |b|^2 with +inf for headroom rows / past the tile's end (one broadcast
         // float4 load per 4 columns); the heap key is only built for survivors
         // of an f32 threshold test against the current K'-th distance.
-        const float thr = top == ~0ull ? INFINITY : __uint_as_float((uint32_t)(top >> 32));
+        // (<= FLT_MAX, not inf: a hit is always finite -- +inf norms never pass)
+        const float thr = top == ~0ull ? 3.402823466e38f : __uint_as_float((uint32_t)(top >> 32));
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
           if (q >= QN) break;
@@ -404,15 +405,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (uint32_t j = 0; j < 16; ++j) {
               const float sc = __shfl_sync(0xFFFFFFFFu, scl, j);  // NaN past c1: fails both tests
-              pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && d[j] < INFINITY && sc >= qlo && sc <= qhi) << j;
+              pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && sc >= qlo && sc <= qhi) << j;
             }
           } else {
-#pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) {
-              const uint32_t c = cb + q * 16 + j;
-              pend |= (uint32_t)(row_ok && ((hit >> j) & 1u) && d[j] < INFINITY && c != prow && c < c1 &&
-                                 !(causal && c > prow)) << j;
-            }
+            // the chunk's admissible columns as one mask: inside the job's span
+            // (warp-uniform), not the row itself, and for causal jobs only
+            // columns before the row
+            const uint32_t cq = cb + q * 16;
+            uint32_t m = c1 > cq ? (c1 - cq >= 16u ? 0xFFFFu : (1u << (c1 - cq)) - 1u) : 0u;
+            if (prow >= cq && prow < cq + 16u) m &= ~(1u << (prow - cq));
+            if (causal) m &= prow < cq ? 0u : (prow - cq >= 15u ? 0xFFFFu : (2u << (prow - cq)) - 1u);
+            pend = row_ok ? (hit & m) : 0u;
           }
           // heap insertions lane-parallel: every lane takes its NEXT survivor in
           // the same pass, so a pass costs one sift-down for all lanes at once
