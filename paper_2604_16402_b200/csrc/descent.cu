@@ -714,22 +714,49 @@ __global__ void k_descent_to_phys(const int32_t* graph, uint32_t n, uint32_t k, 
   const uint32_t lane = lane_id();
   if (w >= (uint64_t)n) return;
   const uint32_t v = (uint32_t)w, pv = s2p[v];
-  for (uint32_t j = 0; j < k; ++j) {
-    const int32_t u = graph[(uint64_t)v * k + j];
-    const bool ok = u >= 0 && (uint32_t)u != v && !isinf(dist[(uint64_t)v * k + j]);  // warp-uniform
-    if (!ok) {
-      if (lane == 0) gf[(uint64_t)pv * k + j] = kSentinel;
-      continue;
+  // 8 edges per round, one f64 partial per edge per lane and reduce_scatter<8>
+  // (the warp_sum tree, bit for bit): 4 rounds of loads in flight instead of 32
+  // dependent ones
+  constexpr int G = 8;
+  for (uint32_t j0 = 0; j0 < k; j0 += G) {
+    uint32_t pu[G];
+    bool ok[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t j = j0 + g;
+      const int32_t u = j < k ? graph[(uint64_t)v * k + j] : -1;
+      ok[g] = u >= 0 && (uint32_t)u != v && !isinf(dist[(uint64_t)v * k + j]);  // warp-uniform
+      pu[g] = ok[g] ? s2p[u] : 0u;
     }
-    const uint32_t pu = s2p[u];
-    double acc = 0.0;
-    for (uint32_t col = lane * 4; col < dp; col += 128)
-      acc = sq4(ldg_nc_f4(X + (uint64_t)pu * dp + col), *reinterpret_cast<const float4*>(X + (uint64_t)pv * dp + col),
-                acc);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      gf[(uint64_t)pv * k + j] = pu;
-      gd[(uint64_t)pv * k + j] = acc;
+    double part[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      double acc = 0.0;
+      if (ok[g])
+        for (uint32_t col = lane * 4; col < dp; col += 128)
+          acc = sq4(ldg_nc_f4(X + (uint64_t)pu[g] * dp + col),
+                    *reinterpret_cast<const float4*>(X + (uint64_t)pv * dp + col), acc);
+      part[g] = acc;
+    }
+    const double sum = reduce_scatter<G>(part);
+    const uint32_t g = lane >> 2;  // lanes 4g .. 4g+3 hold edge j0 + g
+    if ((lane & 3u) == 0 && j0 + g < k) {
+      const uint32_t j = j0 + g;
+      // (ok is warp-uniform per g; pick this lane's edge flags)
+      bool okg = false;
+      uint32_t pug = 0;
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if ((uint32_t)gg == g) {
+          okg = ok[gg];
+          pug = pu[gg];
+        }
+      if (okg) {
+        gf[(uint64_t)pv * k + j] = pug;
+        gd[(uint64_t)pv * k + j] = sum;
+      } else {
+        gf[(uint64_t)pv * k + j] = kSentinel;
+      }
     }
   }
 }
