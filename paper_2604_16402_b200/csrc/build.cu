@@ -909,8 +909,8 @@ void build_index_device(DevIndex& ix, const float* vectors, const float* scalars
   if (mem == GRAB_MEM_HOST) {
     float* x = S.alloc<float>(n * ix.dim);
     float* s = S.alloc<float>(n);
-    GRAB_CUDA(cudaMemcpyAsync(x, vectors, n * ix.dim * 4, cudaMemcpyHostToDevice, st));
     GRAB_CUDA(cudaMemcpyAsync(s, scalars, n * 4, cudaMemcpyHostToDevice, st));
+    upload_h2d(x, vectors, n * ix.dim * 4, st);  // (pinned ring, parallel host copy)
     Xd = x;
     Sd = s;
     std::vector<float> hs(scalars, scalars + n);

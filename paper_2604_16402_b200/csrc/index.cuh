@@ -82,6 +82,11 @@ struct DevIndex {
   size_t device_bytes() const;
 };
 
+// ---- upload.cu ----
+// host -> device copy of a (large, pageable) host buffer, stream-ordered on st;
+// the source may be reused as soon as the call returns
+void upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 // ---- layout.cu ----
 void index_alloc_slots(DevIndex& ix);
 void index_free(DevIndex& ix);
