@@ -547,10 +547,21 @@ __global__ void __launch_bounds__(32 * WPB) k_descent_split(const int32_t* joint
   const uint32_t J = 2 * k;
   const int32_t* jv = joint + (uint64_t)v * J;
   const uint32_t pv = s2p[v];
+  // this node's screen values (nhop * J floats, contiguous) are read only after
+  // the dedup: start pulling them into L2 now
+  if (lane == 0) {
+    const uint32_t bytes = nhop * J * 4;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(buf + (uint64_t)v * nhop * J), "r"(bytes)
+                 : "memory");
+  }
+  // every hop source first (one load per lane), then all their id rows
+  // back to back: the rows' loads are independent and overlap
+  const int32_t src_l = lane < nhop ? jv[hop[lane]] : -1;
   for (uint32_t i = lane; i < H / 2; i += 32) reinterpret_cast<uint32_t*>(hkey)[i] = 0u;
   for (uint32_t i = lane; i < J; i += 32) cid[i] = jointp[(uint64_t)v * J + i];
+#pragma unroll 4
   for (uint32_t h = 0; h < nhop; ++h) {
-    const int32_t src = jv[hop[h]];
+    const int32_t src = __shfl_sync(0xFFFFFFFFu, src_l, h);
     for (uint32_t i = lane; i < J; i += 32) cid[J + h * J + i] = src >= 0 ? jointp[(uint64_t)src * J + i] : -1;
   }
   __syncwarp();
