@@ -25,7 +25,7 @@ from .graph import BucketMeta, GraphIndex, StoreView, create_index
 from .params import BuildParams, DimensionMismatchError, RangePredicate, SearchParams
 
 
-@dataclass
+@dataclass(slots=True)
 class SearchStats:
     """searcher.py:22-31 (+ ``expanded``: frontier nodes popped)."""
 
@@ -40,7 +40,7 @@ class SearchStats:
     elapsed_s: float = 0.0
 
 
-@dataclass
+@dataclass(slots=True)
 class SearchResult:
     """searcher.py:34-49: ascending (distance, slot); ``truncated`` when 0 < len < k."""
 
