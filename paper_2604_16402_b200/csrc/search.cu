@@ -981,8 +981,10 @@ SearchShape make_shape(uint32_t itopk, uint32_t width, uint32_t k_max, uint32_t 
     // per candidate instead of CAS probe chains (measured: 53.8 -> 48.3 ms per
     // 100K candidate searches at 1M rows). Only an interval's own words are
     // ever cleared, so narrow searches pay nothing for the larger allocation.
+    // (GRAB_SEARCH_HASH_VISITED=1 keeps the itopk-sized table, i.e. the hash
+    // path, for wide spans: what indexes above 4M rows always run; tests use it)
     const uint32_t need = ceil_log2(std::max<uint64_t>(1, (phys_rows + 31) / 32));
-    if (need <= 17) s.vlog2 = std::max(s.vlog2, need);
+    if (need <= 17 && !getenv("GRAB_SEARCH_HASH_VISITED")) s.vlog2 = std::max(s.vlog2, need);
     if (const char* e = getenv("GRAB_SEARCH_VLOG2")) s.vlog2 = (uint32_t)atoi(e);  // (lab knob)
   } else {
     // every insert is a distinct in-range row, so the live row count bounds the

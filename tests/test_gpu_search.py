@@ -131,10 +131,17 @@ def _oracle_of(gi):
                            boundaries=meta.boundaries, i2b=meta.index_to_bucket[:n], b2i=meta.bucket_to_index)
 
 
-def test_wide_ranges_use_exact_hash_visited_set(g):
-    """Ranges whose slab interval exceeds the warp's bitmap (here > 131K rows at
-    itopk 64) switch the visited set to the open-addressing hash; results and
-    every SearchStats counter must still equal the oracle (searcher.py:156-233)."""
+@pytest.mark.parametrize("mode", ["hash", "bitmap", "overflow"])
+def test_wide_ranges_use_exact_hash_visited_set(g, mode, monkeypatch):
+    """Ranges whose slab interval exceeds the warp's itopk-sized table (here >
+    131K rows at itopk 64) use the open-addressing hash -- on indexes above 4M
+    rows always, here forced with GRAB_SEARCH_HASH_VISITED -- or, when every phys
+    row fits a bitmap, a full-span bitmap; results and every SearchStats counter
+    must equal the oracle in both modes (searcher.py:156-233)."""
+    if mode in ("hash", "overflow"):
+        monkeypatch.setenv("GRAB_SEARCH_HASH_VISITED", "1")
+    if mode == "overflow":  # a 512-entry table: wide queries pass 3/4 load and are re-run exactly
+        monkeypatch.setenv("GRAB_SEARCH_VLOG2", "9")
     V, S = ist.gen_synthetic(300_000, 16, "gaussian", rng_seed=4)
     gi, _ = g.build_index(V, S, g.BuildParams(k_max=16, k_local=8, bucket_capacity=3000))
     ox = _oracle_of(gi)
