@@ -71,7 +71,11 @@ class GroundTruthCache:
             h.update(struct.pack("<dd", r.lower, r.upper))
         return h.hexdigest()
 
-    def get(self, index, queries, k: int, ranges, live_count: int | None = None) -> list[np.ndarray]:
+    def get(self, store, queries, k: int, ranges, live_count: int | None = None) -> list[np.ndarray]:
+        """evaluate.py:159-182: ``store`` is ``index.store`` as in the reference (a
+        GraphIndex is accepted too); misses run the device brute force on the
+        store's index."""
+        index = store._ix if hasattr(store, "_ix") else store
         store = index.store
         key = self._key(store, queries, k, ranges, live_count)
         if key in self._memo:
@@ -152,7 +156,7 @@ def run_sweep(index, queries, spec: SweepSpec, *, gt_cache: GroundTruthCache | N
     report = EvalReport()
     for sel in spec.selectivities:
         ranges = generate_ranges(scalars, sel, len(queries), spec.rng_seed)
-        truth = cache.get(index, queries, spec.k, ranges)
+        truth = cache.get(index.store, queries, spec.k, ranges)
         lo = np.array([r.lower for r in ranges], dtype=np.float64)
         hi = np.array([r.upper for r in ranges], dtype=np.float64)
         for itopk in spec.itopk_values:

@@ -208,14 +208,40 @@ def insert_golden():
     np.savez_compressed(os.path.join(OUT, "insert.npz"), **out)
 
 
+def sweep_golden():
+    """run_sweep over the small_index fixture (evaluate.py:249-307): the
+    deterministic columns of every grid row, the CSV header, and the GTC1
+    ground-truth files the disk cache wrote (name = SHA-256 key, bytes)."""
+    import tempfile
+    from bucketann import evaluate as ev
+    V, S = ba.gen_synthetic(2000, 8, "clusters", rng_seed=1)
+    index, _ = ba.build_index(V, S, ba.BuildParams(k_max=16, k_local=8, bucket_capacity=250))
+    Q, _ = ba.gen_synthetic(64, 8, "clusters", rng_seed=1)
+    Q = Q + np.float32(0.01)
+    spec = ev.SweepSpec(selectivities=[0.01, 0.1, 0.5, 1.0], itopk_values=[32, 64], search_widths=[1, 4],
+                        max_iterations_values=[10, 50], query_count=48, rng_seed=3)
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        rep = ev.run_sweep(index, Q, spec, gt_cache=ev.GroundTruthCache(d))
+        rep.write_csv(os.path.join(d, "sweep.csv"))
+        out["csv_header"] = np.frombuffer(open(os.path.join(d, "sweep.csv"), "rb").readline(), np.uint8)
+        names = sorted(f for f in os.listdir(d) if f.endswith(".gt"))
+        out["gt_names"] = np.array(names)
+        for i, f in enumerate(names):
+            out[f"gt_{i}"] = np.frombuffer(open(os.path.join(d, f), "rb").read(), np.uint8)
+    cols = ["selectivity", "k", "itopk", "search_width", "max_iterations", "recall", "dist_evals_per_query", "scc"]
+    out["cols"] = np.array(cols)
+    out["rows"] = np.array([[row[c] for c in cols] for row in rep.rows], np.float64)
+    np.savez_compressed(os.path.join(OUT, "sweep.npz"), **out)
+
+
+ALL = ["rng_golden", "layout_golden", "small_golden", "mid_golden", "descent_golden", "insert_golden",
+       "sweep_golden"]
+
 if __name__ == "__main__":
     assert "bucketann" in sys.modules
-    rng_golden()
-    layout_golden()
-    small_golden()
-    mid_golden()
-    descent_golden()
-    insert_golden()
+    for name in (sys.argv[1:] or ALL):
+        globals()[name]()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

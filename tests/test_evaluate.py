@@ -126,3 +126,83 @@ def test_run_sweep_and_cli_end_to_end(tmp_path):
     assert r.returncode == 0 and json.loads(r.stdout)["count"] == 3000
     r = run("analyze", "--index", str(tmp_path / "i.grab"), "--scc")
     assert r.returncode == 0 and int(r.stdout) >= 1
+
+
+SWEEP_SPEC = dict(selectivities=[0.01, 0.1, 0.5, 1.0], itopk_values=[32, 64], search_widths=[1, 4],
+                  max_iterations_values=[10, 50], query_count=48, rng_seed=3)
+
+
+def _sweep_inputs(golden):
+    """small_index fixture + the sweep's queries (tests/golden/make_golden.py:sweep_golden)."""
+    from oracle import index_state as ist
+    gold = golden("small")
+    ref = ist.index_from_container(gold["container"].tobytes())
+    Q, _ = ist.gen_synthetic(64, 8, "clusters", rng_seed=1)
+    return ref, (Q + np.float32(0.01))[:48]
+
+
+def test_sweep_harness_files_match_reference(golden, tmp_path):
+    """The sweep harness's host side against the live reference's run_sweep
+    (evaluate.py:120-307): the ranges of generate_ranges, the GTC1 ground-truth
+    files (SHA-256 key = file name, bytes) and the CSV header are the
+    reference's byte for byte; the deterministic columns (recall,
+    dist_evals_per_query) of the width-4 / 10-iteration cells follow from the
+    oracle's search (a pinned restatement of searcher.py) scored by the
+    product's recall_at_k."""
+    from types import SimpleNamespace
+    from oracle import beam, index_state as ist
+    from paper_2604_16402_b200 import evaluate
+    from paper_2604_16402_b200.datasets import generate_ranges, recall_at_k
+    sw = golden("sweep")
+    ref, Q = _sweep_inputs(golden)
+    n = ref.count
+    store = SimpleNamespace(X=ref.X[:n], scalars=ref.scalars[:n], count=n)
+    cache = evaluate.GroundTruthCache(tmp_path)
+    names = []
+    rows = {tuple(r[:5]): r for r in sw["rows"]}
+    for sel in SWEEP_SPEC["selectivities"]:
+        ranges = generate_ranges(ref.scalars[:n], sel, len(Q), SWEEP_SPEC["rng_seed"])
+        truth = [beam.exact_filtered(ref, q, 10, r.lower, r.upper)[0].astype(np.int64) for q, r in zip(Q, ranges)]
+        key = cache._key(store, Q, 10, ranges, None)
+        cache._write(tmp_path / f"{key}.gt", truth, 10)
+        names.append(f"{key}.gt")
+        rec, ev = [], []
+        for i, (q, r) in enumerate(zip(Q, ranges)):
+            res = beam.beam_search(ref, q, ist.SearchCfg(k=10, lower=r.lower, upper=r.upper, itopk=32, search_width=4,
+                                                         max_iterations=10,
+                                                         rng_seed=beam.derive_seed(SWEEP_SPEC["rng_seed"], i)))
+            rec.append(recall_at_k(res.slots, truth[i], 10))
+            ev.append(res.stats.dist_evals)
+        want = rows[(sel, 10, 32, 4, 10)]
+        assert float(np.nanmean(rec)) == want[5] and float(np.mean(ev)) == want[6], (sel, want)
+    assert sorted(names) == list(sw["gt_names"])
+    for i, name in enumerate(sw["gt_names"]):
+        assert (tmp_path / name).read_bytes() == sw[f"gt_{i}"].tobytes()
+        back = cache._read(tmp_path / name)
+        assert all(t.dtype == np.int64 for t in back)
+    evaluate.EvalReport().write_csv(tmp_path / "empty.csv")
+    assert (tmp_path / "empty.csv").read_bytes() == sw["csv_header"].tobytes()
+
+
+@pytest.mark.gpu
+def test_run_sweep_matches_reference_rows(golden, tmp_path):
+    """run_sweep over the reference-built small_index loaded into the device
+    layout: every grid row's deterministic columns (recall, mean distance
+    evaluations, SCC count) equal the reference's run_sweep, and the disk cache
+    writes the reference's GTC1 files (names and bytes)."""
+    import paper_2604_16402_b200 as g
+    from paper_2604_16402_b200 import evaluate
+    sw = golden("sweep")
+    gold = golden("small")
+    gi = g.load_index(gold["container"].tobytes(), g.BuildParams(k_max=16, k_local=8, bucket_capacity=250))
+    _, Q = _sweep_inputs(golden)
+    rep = evaluate.run_sweep(gi, Q, evaluate.SweepSpec(**SWEEP_SPEC), gt_cache=evaluate.GroundTruthCache(tmp_path))
+    cols = list(sw["cols"])
+    got = np.array([[r[c] for c in cols] for r in rep.rows], np.float64)
+    assert got.shape == sw["rows"].shape
+    assert np.array_equal(got, sw["rows"]), np.argwhere(got != sw["rows"])
+    assert sorted(p.name for p in tmp_path.glob("*.gt")) == list(sw["gt_names"])
+    for i, name in enumerate(sw["gt_names"]):
+        assert (tmp_path / name).read_bytes() == sw[f"gt_{i}"].tobytes()
+    rep.write_csv(tmp_path / "s.csv")
+    assert (tmp_path / "s.csv").read_bytes().startswith(sw["csv_header"].tobytes())
