@@ -2,7 +2,11 @@
 small workload that launches every kernel family (tools/sanitize_workload.py:
 build incl. the tcgen05 screen, search in bitmap / hash modes, brute force,
 insert / rewire / heal, append, phase-level ABI, SCC, sharded pack + merge).
-Each tool must report 0 errors; the logs go to gpurun_out/ for profiles/."""
+Each tool must report 0 errors; the logs go to gpurun_out/ for profiles/.
+
+Opt-in (GRAB_RUN_SANITIZER=1): the GPU pool has since closed compute-sanitizer
+(runs under it left GPUs needing a reset), so the default -m gpu run skips it;
+the clean logs of the round-2 run are in profiles/r02_sanitizer_*.log."""
 import os
 import shutil
 import subprocess
@@ -18,6 +22,8 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_sanitizer_clean(tool):
+    if os.environ.get("GRAB_RUN_SANITIZER") != "1":
+        pytest.skip("opt-in: GRAB_RUN_SANITIZER=1 (compute-sanitizer is closed on the GPU pool)")
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
     env = dict(os.environ, GRAB_NO_ZERO_COPY="1")
@@ -29,6 +35,8 @@ def test_sanitizer_clean(tool):
     if os.path.isdir(logdir):
         with open(os.path.join(logdir, f"sanitizer_{tool}.log"), "w") as f:
             f.write(out)
+    if "compute-sanitizer is closed" in out:
+        pytest.skip(out.strip().splitlines()[0])
     assert "sanitize workload ok" in out, out[-3000:]
     assert r.returncode == 0, out[-3000:]
     clean = "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck" \
