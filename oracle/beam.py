@@ -116,8 +116,19 @@ def _empty(st: Stats) -> Result:
     return Result(np.empty(0, np.int64), np.empty(0, np.float64), False, st)
 
 
+def _visit_stamps(index: OracleIndex) -> tuple[np.ndarray, int]:
+    """searcher.py:90-98: an int64 stamp per row and a per-search epoch (the
+    reference keeps them thread-local; the oracle is single-threaded per process)."""
+    stamps = getattr(index, "_stamps", None)
+    if stamps is None or len(stamps) != len(index.scalars):
+        stamps = index._stamps = np.zeros(len(index.scalars), np.int64)
+        index._epoch = 0
+    index._epoch += 1
+    return stamps, index._epoch
+
+
 def beam_search(index: OracleIndex, query, cfg: SearchCfg, live_count: int | None = None) -> Result:
-    """Alg. 2 (searcher.py:156-233); stamps kept as a Python set (one epoch)."""
+    """Alg. 2 (searcher.py:156-233); visited rows as epoch stamps like the reference."""
     st = Stats()
     n = index.count if live_count is None else live_count
     if n == 0 or index.boundaries is None:
@@ -128,7 +139,8 @@ def beam_search(index: OracleIndex, query, cfg: SearchCfg, live_count: int | Non
     seeds = draw_seeds(index, cfg, lo, hi, n, gen, st)
     if len(seeds) == 0:
         return _empty(st)
-    scored: set[int] = set(seeds.tolist())
+    stamps, epoch = _visit_stamps(index)
+    stamps[seeds] = epoch
     beam = Beam(cfg.itopk)
     beam.admit(seeds, sqdist(q, index.X[seeds]))
     st.dist_evals += len(seeds)
@@ -147,7 +159,7 @@ def beam_search(index: OracleIndex, query, cfg: SearchCfg, live_count: int | Non
         if nb.size == 0:
             continue
         st.gathered += nb.size
-        new = np.fromiter((int(x) not in scored for x in nb), bool, nb.size)
+        new = stamps[nb] != epoch
         ok = (s[nb] >= cfg.lower) & (s[nb] <= cfg.upper)
         st.precheck_rejected += int(np.count_nonzero(new & ~ok))
         elig = nb[new & ok]
@@ -155,7 +167,7 @@ def beam_search(index: OracleIndex, query, cfg: SearchCfg, live_count: int | Non
             continue
         st.in_range_new += elig.size
         st.dist_evals += elig.size
-        scored.update(elig.tolist())
+        stamps[elig] = epoch
         beam.admit(elig, sqdist(q, index.X[elig]))
     k = cfg.k
     out_s, out_d = beam.slots[:k].copy(), beam.dists[:k].copy()
