@@ -44,6 +44,10 @@ GRID = [(32, 1, 50), (32, 2, 50), (48, 2, 50), (64, 2, 50), (64, 4, 50), (96, 4,
         (352, 4, 120), (384, 4, 120), (416, 4, 150), (448, 4, 150), (512, 4, 150), (512, 4, 200)] + [(t, 4, 100) for t in range(264, 352, 8)]
 
 
+# csrc/search.cu kOrderMinQueries: batches with per-query ranges of at least this
+# many queries get one extra launch (k_order_by_lower) before the search grid
+ORDER_MIN_QUERIES = 2048
+
 def env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -575,10 +579,12 @@ def run_sharded(args, cfg, rank, world, local, dist):
                        "exchange": ("peer-memory stores (CUDA IPC over NVLink)" if args.exchange == "p2p"
                                     else "NCCL all_to_all_single") if dist else "none (1 shard)",
                        "global_pass": brep.global_pass},
-            # rank 0, per step: search grid + retry grid, the exchange's pack kernels
-            # (p2p: fill + pack; NCCL: pack, its collective kernels not counted), top-k merge
+            # rank 0, per step: work-order kernel + search grid + retry grid, the exchange's
+            # pack kernels (p2p: fill + pack; NCCL: pack, its collective kernels not
+            # counted), top-k merge
             "build_s": round(build_s, 3),
-            "gpu_launches": args.steps * (2 + (2 if args.exchange == "p2p" else 1) + 1),
+            "gpu_launches": args.steps * ((int(res.routed) >= ORDER_MIN_QUERIES) + 2 +
+                                          (2 if args.exchange == "p2p" else 1) + 1),
             "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line))
@@ -980,8 +986,9 @@ def main():
                          "kernel": "k_search (filtered beam search)",
                          "algorithmic_bytes_per_launch": round(bytes_q), "bytes_per_query": round(bytes_q / nq, 1),
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/search_traffic.json)"},
-            # per step: the search grid + the (normally empty) overflow-retry grid
-            "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "e2e_search_batch": e2e_search_batch,
+            # per step: the work-order kernel (per-query ranges, >= 2048 queries), the
+            # search grid and the (normally empty) overflow-retry grid
+            "gpu_launches": (2 + (nq >= ORDER_MIN_QUERIES)) * args.steps, "clocks": clk.summary(), "e2e_search_batch": e2e_search_batch,
             "timed_instance": "stats-free k_search; bytes from the kernel's counters in a SearchStats run of the "
                               "identical search", "with_search_stats": with_stats,
             "selectivity_sweep": sel_sweep, "sweep": sweep}

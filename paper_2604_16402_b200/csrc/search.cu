@@ -1088,7 +1088,7 @@ static void launch(SearchArgs a, const SearchShape& sh, int num_sms, cudaStream_
 // order makes the reuse safe without host synchronization).
 struct SearchWs {
   std::mutex mu;  // host-side: one enqueue at a time per stream (threads may share a stream)
-  DBufLite tables, big_tables, ovf, ctr;
+  DBufLite tables, big_tables, ovf, ctr, order;
 };
 struct SearchWsCache {
   std::mutex mu;
@@ -1144,6 +1144,83 @@ static void reserve_persisting_l2() {
   cudaGetLastError();  // best effort: never fail a search over the cache reservation
 }
 
+// Work order of a batch with per-query ranges: queries claimed in the order of
+// their lower bound, so the warps resident at any moment search overlapping
+// slab spans and share the rows they read in L2 (random order spreads the
+// resident queries over the whole index). Results are written at the query's
+// own index and every query's search is independent of the order.
+// One block: 2048 bins over [min, max] of the finite lower bounds (unbounded
+// ones go to the end bins), counting sort, order inside a bin arbitrary.
+constexpr uint32_t kOrderBins = 2048, kOrderThreads = 1024;
+
+__global__ void __launch_bounds__(kOrderThreads) k_order_by_lower(const double* lower, uint64_t stride, uint32_t n,
+                                                                  uint32_t* order) {
+  __shared__ uint32_t cnt[kOrderBins];
+  __shared__ float wmin[32], wmax[32];
+  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
+  float mn = INFINITY, mx = -INFINITY;
+  for (uint32_t i = t; i < n; i += kOrderThreads) {
+    const float v = __double2float_rn(lower[(uint64_t)i * stride]);
+    if (isfinite(v)) {
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+  }
+  for (uint32_t o = 16; o; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  }
+  if (lane == 0) {
+    wmin[w] = mn;
+    wmax[w] = mx;
+  }
+  for (uint32_t b = t; b < kOrderBins; b += kOrderThreads) cnt[b] = 0;
+  __syncthreads();
+  mn = wmin[lane];
+  mx = wmax[lane];
+  for (uint32_t o = 16; o; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  }
+  const float scale = mx > mn ? (float)(kOrderBins - 1) / (mx - mn) : 0.f;
+  auto bin_of = [&](uint32_t i) -> uint32_t {
+    const float v = __double2float_rn(lower[(uint64_t)i * stride]);
+    if (!(v >= mn)) return 0;  // -inf (and NaN: any bin is fine)
+    if (!(v <= mx)) return kOrderBins - 1;
+    return min(kOrderBins - 1, (uint32_t)((v - mn) * scale));
+  };
+  for (uint32_t i = t; i < n; i += kOrderThreads) atomicAdd(&cnt[bin_of(i)], 1u);
+  __syncthreads();
+  if (w == 0) {  // exclusive scan of the bins by one warp (64 bins per lane)
+    constexpr uint32_t per = kOrderBins / 32;
+    uint32_t sum = 0;
+    for (uint32_t j = 0; j < per; ++j) sum += cnt[lane * per + j];
+    uint32_t inc = sum;
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += x;
+    }
+    uint32_t run = inc - sum;
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t c = cnt[lane * per + j];
+      cnt[lane * per + j] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < n; i += kOrderThreads) order[atomicAdd(&cnt[bin_of(i)], 1u)] = i;
+}
+
+constexpr uint32_t kOrderMinQueries = 2048;  // smaller batches fit in one wave of resident warps
+
+static const uint32_t* order_by_lower(const SearchArgs& a, SearchWs& ws, cudaStream_t st) {
+  ws.order.ensure((size_t)a.nwork * 4, st);
+  uint32_t* order = (uint32_t*)ws.order.p;
+  k_order_by_lower<<<1, kOrderThreads, 0, st>>>(a.lower, a.range_stride, a.nwork, order);
+  GRAB_CHECK_LAUNCH();
+  return order;
+}
+
 void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   if (a.nwork == 0) return;
   reserve_persisting_l2();
@@ -1169,6 +1246,8 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.ovf_list = ovf + 1;
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
+  static const bool no_order = getenv("GRAB_SEARCH_NO_ORDER") != nullptr;
+  if (a.range_stride != 0 && a.nwork >= kOrderMinQueries && a.work_ctr && !no_order) a.qmap = order_by_lower(a, ws, st);
 #ifdef GRAB_SEARCH_PROFILE
   {
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
