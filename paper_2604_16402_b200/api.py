@@ -67,6 +67,21 @@ class BatchResult:
         return ResultList(self, k)
 
 
+class _BatchItem(SearchResult):
+    """A search_batch result: slots / sq_dists are views of the batch rows and
+    ``stats`` (a SearchStats) is built on first access from the batch's counters,
+    so iterating a 10K-query batch creates one small object per query."""
+
+    __slots__ = ("_src", "_i")
+
+    @property
+    def stats(self) -> SearchStats:
+        return self._src._stats_of(self._i)
+
+
+_new_item = object.__new__
+
+
 class ResultList(Sequence):
     """search_batch's list of SearchResult (searcher.py:236-248), materialised per
     item on access: the batch arrays stay as they came back from the kernel and
@@ -77,17 +92,36 @@ class ResultList(Sequence):
         self._b = batch
         self._k = k
         self._counts = np.asarray(batch.counts).tolist()
-        self._stats = None if batch.stats is None else np.asarray(batch.stats).tolist()
         self._per = batch.elapsed_s / max(len(self._counts), 1)
+        self._stats_rows = None
+        self._full = None  # per-row views of slots / dists (rows with count == k)
 
     def __len__(self) -> int:
         return len(self._counts)
 
+    def _stats_of(self, i: int) -> SearchStats:
+        if self._b.stats is None:
+            return SearchStats(elapsed_s=self._per)
+        if self._stats_rows is None:
+            self._stats_rows = np.asarray(self._b.stats).tolist()
+        return SearchStats(*self._stats_rows[i], elapsed_s=self._per)
+
     def _item(self, i: int) -> SearchResult:
+        if self._full is None:
+            self._full = (list(self._b.slots), list(self._b.dists))
         c = self._counts[i]
-        st = SearchStats(*self._stats[i], elapsed_s=self._per) if self._stats is not None else \
-            SearchStats(elapsed_s=self._per)
-        return SearchResult(self._b.slots[i, :c], self._b.dists[i, :c], 0 < c < self._k, st)
+        r = _new_item(_BatchItem)
+        if c == self._k:
+            r.slots = self._full[0][i]
+            r.sq_dists = self._full[1][i]
+            r.truncated = False
+        else:
+            r.slots = self._b.slots[i, :c]
+            r.sq_dists = self._b.dists[i, :c]
+            r.truncated = 0 < c
+        r._src = self
+        r._i = i
+        return r
 
     def __getitem__(self, i):
         if isinstance(i, slice):

@@ -132,3 +132,36 @@ def test_insert_report_rewired_rows_behave_like_a_sorted_list():
     rep = InsertReport(batch_size=2, rewired_rows=rl)
     assert rep.to_dict()["rewired_rows"] == [3, 7, 7000000, 2 ** 31 + 5]
     assert RowList(np.empty(0, np.uint32)) == [] and len(RowList(np.empty(0, np.uint32))) == 0
+
+
+def test_search_batch_results_are_search_results():
+    """search_batch's ResultList (api.py) against an eagerly built list: every item
+    is a SearchResult whose slots / sq_dists / truncated / stats are the batch
+    row's (searcher.py:34-49), including short (truncated) and empty rows."""
+    import numpy as np
+    from paper_2604_16402_b200.api import BatchResult, SearchResult, SearchStats
+    nq, k = 7, 4
+    names = ["iterations", "dist_evals", "seed_evals", "gathered", "in_range_new", "precheck_rejected",
+             "seed_attempts", "expanded"]
+    st = np.zeros(nq, dtype=[(f, "<u4") for f in names])
+    for j, f in enumerate(names):
+        st[f] = np.arange(nq) * 10 + j
+    counts = np.array([4, 2, 0, 4, 1, 4, 3], np.uint32)
+    slots = np.arange(nq * k, dtype=np.int64).reshape(nq, k)
+    dists = slots.astype(np.float64) / 3
+    rs = BatchResult(slots, dists, counts, st, 0.7).to_results(k)
+    assert len(rs) == nq
+    for i, r in enumerate(rs):
+        c = int(counts[i])
+        want = SearchResult(slots[i, :c], dists[i, :c], 0 < c < k,
+                            SearchStats(*[int(st[f][i]) for f in names], elapsed_s=0.7 / nq))
+        assert isinstance(r, SearchResult)
+        assert np.array_equal(r.slots, want.slots) and np.array_equal(r.sq_dists, want.sq_dists)
+        assert r.truncated == want.truncated and len(r) == c
+        assert r.stats == want.stats
+    assert rs[-1].stats.dist_evals == rs[6].stats.dist_evals == 61
+    assert [len(r) for r in rs[1:4]] == [2, 0, 4]
+    with pytest.raises(IndexError):
+        rs[nq]
+    nostats = BatchResult(slots, dists, counts, None, 0.7).to_results(k)
+    assert nostats[0].stats == SearchStats(elapsed_s=0.7 / nq)
