@@ -1213,6 +1213,116 @@ __global__ void __launch_bounds__(kOrderThreads) k_order_by_lower(const double* 
 
 constexpr uint32_t kOrderMinQueries = 2048;  // smaller batches fit in one wave of resident warps
 
+// Work order of a batch with ONE shared range (search_batch, the insert's
+// full-range candidate search): queries grouped by where they lie in vector
+// space, so resident warps walk overlapping graph neighbourhoods and share the
+// rows they read in L2. Cell = signs of kSimBits random +-1 projections, each
+// taken relative to the batch mean of that projection; cells sorted as integers
+// (the first projections are the coarsest split).
+constexpr uint32_t kSimBits = 10;
+
+__device__ __forceinline__ uint32_t sim_hash(uint32_t x) {  // lowbias32
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+// warp per query: proj[q][j] = sum_c x[c] * (+-1), sign bit `lane` of hash(j, c / 32)
+__global__ void k_sim_project(const float* Q, const uint32_t* qphys, const float* X, uint32_t dp, uint32_t n,
+                              float* proj, float* sums) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  float tot[kSimBits];
+#pragma unroll
+  for (uint32_t j = 0; j < kSimBits; ++j) tot[j] = 0.f;
+  for (uint32_t q = w0; q < n; q += nw) {
+    const float* row = qphys ? X + (uint64_t)qphys[q] * dp : Q + (uint64_t)q * dp;
+    float acc[kSimBits];
+#pragma unroll
+    for (uint32_t j = 0; j < kSimBits; ++j) acc[j] = 0.f;
+    for (uint32_t c = lane, i = 0; c < dp; c += 32, ++i) {
+      const float x = __ldg(row + c);
+#pragma unroll
+      for (uint32_t j = 0; j < kSimBits; ++j)
+        acc[j] += ((sim_hash(j * 4096u + i) >> lane) & 1u) ? x : -x;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kSimBits; ++j) {
+      float v = acc[j];
+      for (uint32_t o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      acc[j] = v;
+      tot[j] += v;
+    }
+    if (lane < kSimBits) {
+      float mine = acc[0];
+#pragma unroll
+      for (uint32_t j = 1; j < kSimBits; ++j) mine = lane == j ? acc[j] : mine;
+      proj[(uint64_t)q * kSimBits + lane] = mine;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (uint32_t j = 0; j < kSimBits; ++j) atomicAdd(&sums[j], tot[j]);
+  }
+}
+
+// one block: counting sort of the queries by cell
+__global__ void __launch_bounds__(kOrderThreads) k_order_by_cell(const float* proj, const float* sums, uint32_t n,
+                                                                 uint32_t* order) {
+  constexpr uint32_t NB = 1u << kSimBits;
+  __shared__ uint32_t cnt[NB];
+  __shared__ float mean[kSimBits];
+  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t < kSimBits) mean[t] = sums[t] / (float)n;
+  for (uint32_t b = t; b < NB; b += kOrderThreads) cnt[b] = 0;
+  __syncthreads();
+  auto cell = [&](uint32_t q) -> uint32_t {
+    uint32_t c = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kSimBits; ++j) c = (c << 1) | (proj[(uint64_t)q * kSimBits + j] > mean[j] ? 1u : 0u);
+    return c;
+  };
+  for (uint32_t q = t; q < n; q += kOrderThreads) atomicAdd(&cnt[cell(q)], 1u);
+  __syncthreads();
+  if (w == 0) {
+    constexpr uint32_t per = NB / 32;
+    uint32_t sum = 0;
+    for (uint32_t j = 0; j < per; ++j) sum += cnt[lane * per + j];
+    uint32_t inc = sum;
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += x;
+    }
+    uint32_t run = inc - sum;
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t c = cnt[lane * per + j];
+      cnt[lane * per + j] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (uint32_t q = t; q < n; q += kOrderThreads) order[atomicAdd(&cnt[cell(q)], 1u)] = q;
+}
+
+static const uint32_t* order_by_cell(const DevIndex& ix, const SearchArgs& a, SearchWs& ws, cudaStream_t st) {
+  const uint32_t n = a.nwork;
+  const size_t o_order = 0, o_proj = ((size_t)n * 4 + 255) / 256 * 256;
+  const size_t o_sums = o_proj + ((size_t)n * kSimBits * 4 + 255) / 256 * 256;
+  ws.order.ensure(o_sums + 64, st);
+  uint8_t* p = (uint8_t*)ws.order.p;
+  float* sums = (float*)(p + o_sums);
+  GRAB_CUDA(cudaMemsetAsync(sums, 0, kSimBits * 4, st));
+  const unsigned blocks = (unsigned)std::min<uint64_t>(div_up(n, 8), 4ull * ix.num_sms);
+  k_sim_project<<<blocks, 256, 0, st>>>(a.Q, a.qphys, a.X, a.dp, n, (float*)(p + o_proj), sums);
+  GRAB_CHECK_LAUNCH();
+  k_order_by_cell<<<1, kOrderThreads, 0, st>>>((const float*)(p + o_proj), sums, n, (uint32_t*)(p + o_order));
+  GRAB_CHECK_LAUNCH();
+  return (const uint32_t*)(p + o_order);
+}
+
 static const uint32_t* order_by_lower(const SearchArgs& a, SearchWs& ws, cudaStream_t st) {
   ws.order.ensure((size_t)a.nwork * 4, st);
   uint32_t* order = (uint32_t*)ws.order.p;
@@ -1247,7 +1357,11 @@ void run_search(const DevIndex& ix, SearchArgs a, cudaStream_t st) {
   a.qmap = nullptr;
   a.nwork_dev = nullptr;
   static const bool no_order = getenv("GRAB_SEARCH_NO_ORDER") != nullptr;
-  if (a.range_stride != 0 && a.nwork >= kOrderMinQueries && a.work_ctr && !no_order) a.qmap = order_by_lower(a, ws, st);
+  static const bool no_sim = getenv("GRAB_SEARCH_NO_SIM_ORDER") != nullptr;
+  if (a.nwork >= kOrderMinQueries && a.work_ctr && !no_order) {
+    if (a.range_stride != 0) a.qmap = order_by_lower(a, ws, st);
+    else if (!no_sim) a.qmap = order_by_cell(ix, a, ws, st);
+  }
 #ifdef GRAB_SEARCH_PROFILE
   {
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
