@@ -111,3 +111,32 @@ def test_insert_every_newcomer_reachable_and_capacity_error(g):
     with pytest.raises(g.CapacityError):
         g.insert_batch(gi, X[:200], S[:200])
     assert gi.count == 6_600
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_work_order_does_not_change_results(g, built, shared):
+    """Batches of >= 2048 queries are claimed in a work order (per-query ranges:
+    by lower bound, k_order_by_lower; one shared range: by LSH cell,
+    k_sim_project / k_order_by_cell -- csrc/search.cu). Every query's search is
+    independent of the order: the batch equals the same queries run in
+    512-query chunks (below the threshold: claimed in index order) with the same
+    per-query seeds -- slots, f64 distances, counts and every counter."""
+    gi, X, S = built
+    nq = 3000
+    Q = ist.lowrank_queries(nq, 32, seed=33)
+    if shared:
+        lo, hi = np.float64(0.2), np.float64(0.7)
+    else:
+        r = beam.window_ranges(S, 0.1, nq, 9)
+        lo = np.array([a for a, _ in r])
+        hi = np.array([b for _, b in r])
+    p = g.SearchParams(k=10, itopk=96)
+    whole = g.search_arrays(gi, Q, lo, hi, p, seed_base=5)
+    for c0 in range(0, nq, 512):
+        sl = slice(c0, min(nq, c0 + 512))
+        part = g.search_arrays(gi, Q[sl], lo if shared else lo[sl], hi if shared else hi[sl], p, seed_base=5,
+                               ordinal0=c0)
+        assert np.array_equal(part.slots, whole.slots[sl])
+        assert np.array_equal(part.dists, whole.dists[sl], equal_nan=True)
+        assert np.array_equal(part.counts, whole.counts[sl])
+        assert np.array_equal(part.stats, whole.stats[sl])
