@@ -630,7 +630,10 @@ def run_reference_arm(args, cfg, local):
     steps = args.steps
     qps, el, _ = cpu_search_qps(idx, Q, lo, hi, seeds, (itopk, width, iters), procs, steps, args.warmup)
     line = {"impl": "reference", "metric": "range-filtered QPS @ recall@10=0.95", "value": round(qps, 2),
-            "unit": "queries/s", "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": el / steps * 1e3,
+            # n_gpus = the launch's N (the driver pairs lines per N); the work is rank 0's
+            # host cores alone -- the reference has no GPU or multi-process path
+            "unit": "queries/s", "n_gpus": args.gpus, "host_only": True, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": el / steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": meta["config"],
             "cpu_baseline": {"value": round(qps, 2), "unit": "queries/s", "cores": procs, "kind": "port",
