@@ -443,6 +443,24 @@ __global__ void k_count_src(const uint32_t* key, uint64_t m, uint32_t n, uint32_
   if (i < m && key[i] < n) atomicAdd(cnt + key[i], 1u);
 }
 
+// Packed FP32 pairs (Blackwell FADD2 / FFMA2): one instruction works on two
+// dimensions, so the screen's even and odd dimensions accumulate in the two
+// halves of a 64-bit register and are added at the end (a two-way split of the
+// sum: its rounding bound is below the sequential one the margin `gam` covers).
+__device__ __forceinline__ uint64_t f32x2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f32x2_fma_sq(uint64_t d, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(d), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float f32x2_hsum(uint64_t v) {
+  return __uint_as_float((uint32_t)v) + __uint_as_float((uint32_t)(v >> 32));
+}
+
 // Block per source u (8 warps): warp w takes users 2w, 2w+1 of a 16-user chunk,
 // lane l candidates l and l + 32; 128-float dimension chunks staged with a
 // padded stride (conflict-free float4 reads).
@@ -479,7 +497,7 @@ __global__ void __launch_bounds__(256) k_hop_dists(const uint32_t* off, const ui
       upair[tid] = pr;
       uph[tid] = tid < nu ? s2p[pr / nhop] : 0u;
     }
-    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    uint64_t acc[2][2] = {{0ull, 0ull}, {0ull, 0ull}};  // (even, odd) dimension partial sums
     for (uint32_t d0 = 0; d0 < dp; d0 += 128) {
       __syncthreads();
       if (!one_chunk) load_cand(d0);
@@ -497,21 +515,18 @@ __global__ void __launch_bounds__(256) k_hop_dists(const uint32_t* off, const ui
       const float* ubr = usr + (2 * w + 1) * kHopPad;
 #pragma unroll 4
       for (uint32_t f = 0; f < dl; f += 4) {
-        const float4 xa = *reinterpret_cast<const float4*>(ca + f);
-        const float4 xb = *reinterpret_cast<const float4*>(cb + f);
-        const float4 qa = *reinterpret_cast<const float4*>(ua + f);
-        const float4 qb = *reinterpret_cast<const float4*>(ubr + f);
-        const float xv[2][4] = {{xa.x, xa.y, xa.z, xa.w}, {xb.x, xb.y, xb.z, xb.w}};
-        const float qv[2][4] = {{qa.x, qa.y, qa.z, qa.w}, {qb.x, qb.y, qb.z, qb.w}};
+        const ulonglong2 xa = *reinterpret_cast<const ulonglong2*>(ca + f);
+        const ulonglong2 xb = *reinterpret_cast<const ulonglong2*>(cb + f);
+        const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(ua + f);
+        const ulonglong2 qb = *reinterpret_cast<const ulonglong2*>(ubr + f);
+        const uint64_t xv[2][2] = {{xa.x, xa.y}, {xb.x, xb.y}};
+        const uint64_t qv[2][2] = {{qa.x, qa.y}, {qb.x, qb.y}};
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const float df = xv[j][t] - qv[i][t];
-              acc[i][j] = fmaf(df, df, acc[i][j]);
-            }
+            for (int j = 0; j < 2; ++j) acc[i][j] = f32x2_fma_sq(f32x2_sub(xv[j][t], qv[i][t]), acc[i][j]);
       }
     }
 #pragma unroll
@@ -520,8 +535,8 @@ __global__ void __launch_bounds__(256) k_hop_dists(const uint32_t* off, const ui
       if (ui >= nu) continue;
       float* row = buf + (uint64_t)upair[ui] * J;  // pair index v * nhop + h
       const float kInfF = __int_as_float(0x7F800000);
-      if (c0 < J) row[c0] = cph[c0] >= 0 ? acc[i][0] : kInfF;
-      if (c1 < J) row[c1] = cph[c1] >= 0 ? acc[i][1] : kInfF;
+      if (c0 < J) row[c0] = cph[c0] >= 0 ? f32x2_hsum(acc[i][0]) : kInfF;
+      if (c1 < J) row[c1] = cph[c1] >= 0 ? f32x2_hsum(acc[i][1]) : kInfF;
     }
   }
 }
