@@ -85,53 +85,37 @@ __device__ __forceinline__ double warp_sum(double v) {
 // with the full sum of candidate (i >> (5 - log2 G)); bit-identical to
 // warp_sum(p[g]) because every level adds the same operand pair.
 // Shuffles: 18 (G=8), 20 (G=4), 18 (G=2) double-words vs 10*G for warp_sum.
+// One level per halving (i^16 splits G -> G/2, i^8 G/2 -> G/4, ...), the
+// remaining levels all-reduce.
+template <int N, uint32_t OFF>
+__device__ __forceinline__ double reduce_scatter_level(const double (&p)[N]) {
+  const uint32_t lane = threadIdx.x & 31u;
+  constexpr int H = N / 2;
+  const bool hi = (lane & OFF) != 0;
+  double q[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    const double send = hi ? p[j] : p[H + j];
+    const double keep = hi ? p[H + j] : p[j];
+    q[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, OFF);
+  }
+  if constexpr (H == 1) {
+    double t = q[0];
+#pragma unroll
+    for (uint32_t o = OFF / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+    return t;
+  } else {
+    return reduce_scatter_level<H, OFF / 2>(q);
+  }
+}
+
 template <int G>
 __device__ __forceinline__ double reduce_scatter(double (&p)[G]) {
-  const uint32_t lane = threadIdx.x & 31u;
+  static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "G: a power of two <= 16");
   if constexpr (G == 1) {
     return warp_sum(p[0]);
   } else {
-    constexpr int H = G / 2;
-    constexpr uint32_t OFF = 16;
-    const bool hi = (lane & OFF) != 0;
-    double q[H];
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
-      const double send = hi ? p[j] : p[H + j];
-      const double keep = hi ? p[H + j] : p[j];
-      q[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, OFF);
-    }
-    if constexpr (H == 1) {
-      double t = q[0];
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
-      return t;
-    } else {
-      constexpr int H2 = H / 2;
-      const bool hi2 = (lane & 8u) != 0;
-      double r[H2];
-#pragma unroll
-      for (int j = 0; j < H2; ++j) {
-        const double send = hi2 ? q[j] : q[H2 + j];
-        const double keep = hi2 ? q[H2 + j] : q[j];
-        r[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 8);
-      }
-      if constexpr (H2 == 1) {
-        double t = r[0];
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
-        return t;
-      } else {
-        static_assert(H2 == 2, "G <= 8");
-        const bool hi3 = (lane & 4u) != 0;
-        const double send = hi3 ? r[0] : r[1];
-        const double keep = hi3 ? r[1] : r[0];
-        double t = keep + __shfl_xor_sync(0xFFFFFFFFu, send, 4);
-        t += __shfl_xor_sync(0xFFFFFFFFu, t, 2);
-        t += __shfl_xor_sync(0xFFFFFFFFu, t, 1);
-        return t;
-      }
-    }
+    return reduce_scatter_level<G, 16>(p);
   }
 }
 

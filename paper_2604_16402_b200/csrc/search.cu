@@ -212,7 +212,7 @@ __host__ __device__ inline WarpLayout warp_layout(const SearchShape& s) {
   l.cs = o;
   o += align16(s.cmax * 4);
   l.cp = o;
-  o += align16((s.cmax + 8) * 4);
+  o += align16((s.cmax + 16) * 4);  // + a round of padding (pad_cands)
   l.dd = o;
   o += align16(s.dsz * 4);
   l.fr = o;
@@ -338,12 +338,12 @@ __device__ __forceinline__ void score(const QueryRegs<NC>& qr, const float* __re
   __syncwarp();
 }
 
-// Pad cp[n .. n+8) with cp[0] so score() can issue whole rounds.
+// Pad cp[n .. n+16) with cp[0] so score() can issue whole rounds (G <= 16).
 __device__ __forceinline__ void pad_cands(uint32_t* cp, uint32_t n) {
   __syncwarp();
   const uint32_t lane = lane_id();
   const uint32_t p0 = cp[0];
-  if (lane < 8) cp[n + lane] = p0;
+  if (lane < 16) cp[n + lane] = p0;
   __syncwarp();
 }
 
