@@ -375,26 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // of an f32 threshold test against the current K'-th distance.
         // (<= FLT_MAX, not inf: a hit is always finite -- +inf norms never pass)
         const float thr = top == ~0ull ? 3.402823466e38f : __uint_as_float((uint32_t)(top >> 32));
-#pragma unroll
-        for (uint32_t q = 0; q < 4; ++q) {
-          if (q >= QN) break;
-          // branch-free pass over 16 columns: distances + survivor mask
-          float d[16];
-          uint32_t hit = 0;
-#pragma unroll
-          for (uint32_t j4 = 0; j4 < 4; ++j4) {
-            const float4 n4 = __ldg(reinterpret_cast<const float4*>(norms + cb + q * 16) + j4);
-            const float b2[4] = {n4.x, n4.y, n4.z, n4.w};
-#pragma unroll
-            for (uint32_t u = 0; u < 4; ++u) {
-              const uint32_t j = 4 * j4 + u;
-              d[j] = fmaxf(fmaf(-2.f, __uint_as_float(v[q][j]), a2 + b2[u]), 0.f);
-              hit |= (uint32_t)(d[j] <= thr) << j;
-            }
-          }
-          if (!__any_sync(0xFFFFFFFFu, hit != 0u)) continue;  // the common case after the first tiles
-          // admissible survivors of this chunk (finite, not the row itself, in
-          // range, causal for insert candidates)
+        // admissible survivors of chunk q (finite, not the row itself, in range,
+        // causal for insert candidates) among its threshold hits
+        auto chunk_pend = [&](uint32_t q, uint32_t hit) -> uint32_t {
           uint32_t pend = 0;
           if constexpr (BF) {
             // the row's own range on the column's scalar: lane j loads column j's
@@ -417,18 +400,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (causal) m &= prow < cq ? 0u : (prow - cq >= 15u ? 0xFFFFu : (2u << (prow - cq)) - 1u);
             pend = row_ok ? (hit & m) : 0u;
           }
+          return pend;
+        };
+        // chunks in pairs: one insertion loop per 32 columns, so a pass serves
+        // the survivors of both chunks (the loop runs max-over-lanes survivors
+        // of the pair instead of the sum of the two chunks' maxima)
+#pragma unroll
+        for (uint32_t qp = 0; qp < 2; ++qp) {
+          if (2 * qp >= QN) break;
+          // branch-free pass over 32 columns: distances + survivor masks
+          float d[2][16];
+          uint32_t hit[2] = {0u, 0u};
+#pragma unroll
+          for (uint32_t h2 = 0; h2 < 2; ++h2) {
+            const uint32_t q = 2 * qp + h2;
+#pragma unroll
+            for (uint32_t j4 = 0; j4 < 4; ++j4) {
+              const float4 n4 = __ldg(reinterpret_cast<const float4*>(norms + cb + q * 16) + j4);
+              const float b2[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+              for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * j4 + u;
+                d[h2][j] = fmaxf(fmaf(-2.f, __uint_as_float(v[q][j]), a2 + b2[u]), 0.f);
+                hit[h2] |= (uint32_t)(d[h2][j] <= thr) << j;
+              }
+            }
+          }
+          if (!__any_sync(0xFFFFFFFFu, (hit[0] | hit[1]) != 0u)) continue;  // the common case after the first tiles
+          uint32_t pend = 0;
+          if (__any_sync(0xFFFFFFFFu, hit[0] != 0u)) pend = chunk_pend(2 * qp, hit[0]);
+          if (__any_sync(0xFFFFFFFFu, hit[1] != 0u)) pend |= chunk_pend(2 * qp + 1, hit[1]) << 16;
           // heap insertions lane-parallel: every lane takes its NEXT survivor in
           // the same pass, so a pass costs one sift-down for all lanes at once
           // (a per-column loop would run one pass per distinct hit column);
           // per row the keys still arrive in column order
           while (__any_sync(0xFFFFFFFFu, pend != 0u)) {
             if (pend) {
-              const uint32_t j = __ffs(pend) - 1;
+              const uint32_t jb = __ffs(pend) - 1;
               pend &= pend - 1;
-              float dj = d[0];
+              const bool hi = jb >= 16;
+              const uint32_t j = jb & 15;
+              float dj = hi ? d[1][0] : d[0][0];
 #pragma unroll
-              for (uint32_t jj = 1; jj < 16; ++jj) dj = j == jj ? d[jj] : dj;
-              const uint64_t key = ((uint64_t)__float_as_uint(dj) << 32) | (cb + q * 16 + j);
+              for (uint32_t jj = 1; jj < 16; ++jj) dj = j == jj ? (hi ? d[1][jj] : d[0][jj]) : dj;
+              const uint64_t key = ((uint64_t)__float_as_uint(dj) << 32) | (cb + 2 * qp * 16 + jb);
               if (key < top) {
                 heap_replace_top(h, KP, key);
                 top = h[0];
