@@ -438,11 +438,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (pend) {
               const uint32_t jb = __ffs(pend) - 1;
               pend &= pend - 1;
-              const bool hi = jb >= 16;
-              const uint32_t j = jb & 15;
-              float dj = hi ? d[1][0] : d[0][0];
+              // d[jb] by a binary select tree on jb's bits (31 selects, no compares)
+              float t16[16], t8[8], t4[4];
 #pragma unroll
-              for (uint32_t jj = 1; jj < 16; ++jj) dj = j == jj ? (hi ? d[1][jj] : d[0][jj]) : dj;
+              for (uint32_t i = 0; i < 16; ++i) t16[i] = (jb & 1u) ? d[i >> 3][((2 * i) & 15) + 1] : d[i >> 3][(2 * i) & 15];
+#pragma unroll
+              for (uint32_t i = 0; i < 8; ++i) t8[i] = (jb & 2u) ? t16[2 * i + 1] : t16[2 * i];
+#pragma unroll
+              for (uint32_t i = 0; i < 4; ++i) t4[i] = (jb & 4u) ? t8[2 * i + 1] : t8[2 * i];
+              const float t2a = (jb & 8u) ? t4[1] : t4[0], t2b = (jb & 8u) ? t4[3] : t4[2];
+              const float dj = (jb & 16u) ? t2b : t2a;
               const uint64_t key = ((uint64_t)__float_as_uint(dj) << 32) | (cb + 2 * qp * 16 + jb);
               if (key < top) {
                 heap_replace_top(h, KP, key);
