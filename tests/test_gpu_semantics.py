@@ -143,3 +143,32 @@ def test_work_order_does_not_change_results(g, built, shared):
         assert np.array_equal(part.dists, whole.dists[sl], equal_nan=True)
         assert np.array_equal(part.counts, whole.counts[sl])
         assert np.array_equal(part.stats, whole.stats[sl])
+
+
+def test_work_order_with_invalid_device_bounds(g, built):
+    """Device-resident bounds skip the host's lower <= upper check: inverted and
+    NaN ranges reach the ordering kernel and the search kernel, which give those
+    queries an empty result; every other query of the (ordered) batch returns
+    what it returns alone."""
+    import torch
+    gi, X, S = built
+    nq = 2500
+    Q = ist.lowrank_queries(nq, 32, seed=34)
+    r = beam.window_ranges(S, 0.1, nq, 10)
+    lo = np.array([a for a, _ in r])
+    hi = np.array([b for _, b in r])
+    bad = np.zeros(nq, bool)
+    bad[5:200:7] = True
+    lo[5:200:14], hi[5:200:14] = hi[5:200:14], lo[5:200:14]  # inverted
+    lo[12:200:14] = np.nan
+    seeds = (np.arange(nq, dtype=np.uint64) * np.uint64(7919) + np.uint64(5))
+    p = g.SearchParams(k=10, itopk=96)
+    dev = torch.device("cuda", gi.device)
+    res = g.search_arrays(gi, torch.from_numpy(Q).to(dev), torch.from_numpy(lo).to(dev),
+                          torch.from_numpy(hi).to(dev), p, seeds=torch.from_numpy(seeds.view(np.int64)).to(dev))
+    counts = res.counts.cpu().numpy()
+    assert (counts[bad] == 0).all()
+    good = ~bad
+    alone = g.search_arrays(gi, Q[good], lo[good], hi[good], p, seeds=seeds[good])
+    assert np.array_equal(res.slots.cpu().numpy()[good], alone.slots)
+    assert np.array_equal(counts[good], alone.counts)
