@@ -1153,17 +1153,33 @@ static void reserve_persisting_l2() {
 // ones go to the end bins), counting sort, order inside a bin arbitrary.
 constexpr uint32_t kOrderBins = 2048, kOrderThreads = 1024;
 
+// `lower` may be page-locked host memory (the zero-copy path): it is read
+// once, 8 loads in flight per thread, into the device copy `lf` that the
+// histogram and scatter passes use.
 __global__ void __launch_bounds__(kOrderThreads) k_order_by_lower(const double* lower, uint64_t stride, uint32_t n,
-                                                                  uint32_t* order) {
+                                                                  float* lf, uint32_t* order) {
   __shared__ uint32_t cnt[kOrderBins];
   __shared__ float wmin[32], wmax[32];
   const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
   float mn = INFINITY, mx = -INFINITY;
-  for (uint32_t i = t; i < n; i += kOrderThreads) {
-    const float v = __double2float_rn(lower[(uint64_t)i * stride]);
-    if (isfinite(v)) {
-      mn = fminf(mn, v);
-      mx = fmaxf(mx, v);
+  constexpr uint32_t B = 8;
+  for (uint32_t i0 = t; i0 < n; i0 += B * kOrderThreads) {
+    double x[B];
+#pragma unroll
+    for (uint32_t b = 0; b < B; ++b) {
+      const uint32_t i = i0 + b * kOrderThreads;
+      x[b] = i < n ? lower[(uint64_t)i * stride] : 0.0;
+    }
+#pragma unroll
+    for (uint32_t b = 0; b < B; ++b) {
+      const uint32_t i = i0 + b * kOrderThreads;
+      if (i >= n) break;
+      const float v = __double2float_rn(x[b]);
+      lf[i] = v;
+      if (isfinite(v)) {
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+      }
     }
   }
   for (uint32_t o = 16; o; o >>= 1) {
@@ -1184,7 +1200,7 @@ __global__ void __launch_bounds__(kOrderThreads) k_order_by_lower(const double* 
   }
   const float scale = mx > mn ? (float)(kOrderBins - 1) / (mx - mn) : 0.f;
   auto bin_of = [&](uint32_t i) -> uint32_t {
-    const float v = __double2float_rn(lower[(uint64_t)i * stride]);
+    const float v = lf[i];  // written by this thread in the first pass (same i -> same thread)
     if (!(v >= mn)) return 0;  // -inf (and NaN: any bin is fine)
     if (!(v <= mx)) return kOrderBins - 1;
     return min(kOrderBins - 1, (uint32_t)((v - mn) * scale));
@@ -1324,9 +1340,9 @@ static const uint32_t* order_by_cell(const DevIndex& ix, const SearchArgs& a, Se
 }
 
 static const uint32_t* order_by_lower(const SearchArgs& a, SearchWs& ws, cudaStream_t st) {
-  ws.order.ensure((size_t)a.nwork * 4, st);
+  ws.order.ensure((size_t)a.nwork * 8, st);
   uint32_t* order = (uint32_t*)ws.order.p;
-  k_order_by_lower<<<1, kOrderThreads, 0, st>>>(a.lower, a.range_stride, a.nwork, order);
+  k_order_by_lower<<<1, kOrderThreads, 0, st>>>(a.lower, a.range_stride, a.nwork, (float*)(order + a.nwork), order);
   GRAB_CHECK_LAUNCH();
   return order;
 }
